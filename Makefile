@@ -1,0 +1,44 @@
+# Build of the B200 hot path (sm_100a only) and the test oracles.
+#
+#   make            -> paper_1502_03391_b200/libjofc_gpu.so (C ABI + kernels)
+#                      paper_1502_03391_b200/libjofc.so     (C++ drop-in, namespace jofc)
+#                      oracle/libjofc_oracle.so             (test oracle, C restatement)
+#   make ref        -> oracle/_ref/libjofc_ref.so           (needs /root/reference)
+NVCC    ?= /usr/local/cuda/bin/nvcc
+CXX     := /usr/bin/g++
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+PKG     := paper_1502_03391_b200
+CSRC    := $(PKG)/csrc
+NVFLAGS := $(EXTRA) -O3 -std=c++17 $(ARCH) -lineinfo -Iinclude -I$(CSRC) \
+           -Xcompiler -fPIC,-fopenmp,-Wall -ccbin $(CXX)
+GPU_SRC := $(CSRC)/jofc_capi.cu $(CSRC)/jofc_weights.cpp $(CSRC)/workloads.cpp
+GPU_HDR := $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/jofc_gpu.h include/jofc_workloads.h
+DROPIN_SRC := $(wildcard $(CSRC)/dropin/*.cpp)
+DROPIN_HDR := $(wildcard include/jofc/*.hpp)
+
+all: $(PKG)/libjofc_gpu.so $(PKG)/libjofc_probe.so oracle
+
+$(PKG)/libjofc_probe.so: $(CSRC)/probe.cu
+	$(NVCC) $(NVFLAGS) -shared -o $@ $<
+
+$(PKG)/libjofc_gpu.so: $(GPU_SRC) $(GPU_HDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPU_SRC) -lgomp
+
+$(PKG)/libjofc.so: $(DROPIN_SRC) $(DROPIN_HDR) $(PKG)/libjofc_gpu.so
+	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(DROPIN_SRC) \
+	    -L$(PKG) -ljofc_gpu -Wl,-rpath,'$$ORIGIN'
+
+oracle:
+	$(MAKE) -C oracle all
+
+ref:
+	$(MAKE) -C oracle ref
+
+sass: $(PKG)/libjofc_gpu.so
+	/usr/local/cuda/bin/cuobjdump -sass $< > build_sass.txt
+
+clean:
+	rm -f $(PKG)/*.so
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle ref sass clean

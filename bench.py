@@ -1,0 +1,455 @@
+#!/usr/bin/env python
+"""bench.py -- fJOFC Guttman loop on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+One step = one full fJOFC solve of the chosen config (BASELINE.json configs;
+default config 3: m=2, n=20000, d=5, w=0.5, 100 Guttman iterations, the
+config the 1/2/4/8-GPU metric is quoted on).  `value` = Guttman iterations/s
+over the whole job (iterations x steps / max-over-ranks device time) with the
+packed Delta resident in HBM; `e2e` = the same metric through the C ABI
+(jofc_set_problem from pinned host dense Delta + jofc_fjofc_embed with host
+X0/X/trace), copies inside the timed region.  Multi-GPU (torchrun): Delta's
+packed tile stream is split into balanced contiguous shards; each iteration
+all-reduces the m*n*d partial product (+ fidelity) with NCCL; strong scaling.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libjofc_ref.so, the unmodified reference sources; the C
+restatement when that was not built) on the same workload, all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_NAMES = {1: "C1", 2: "C2", 3: "C3", 4: "C4", 5: "C5-in"}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def probe_fp64(device):
+    import ctypes as C
+    lib = C.CDLL(os.path.join(ROOT, "paper_1502_03391_b200", "libjofc_probe.so"))
+    a, b, c = C.c_double(), C.c_double(), C.c_double()
+    if lib.jofc_probe_fp64(int(device), C.byref(a), C.byref(b), C.byref(c)) != 0:
+        return None
+    return {"dfma_tflops": a.value, "dmma_tflops": b.value, "mixed_tflops": c.value}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def h2d_bytes_dense_upload(m, n, world, rank):
+    """Bytes jofc_set_problem copies: 8-band row chunks, columns from the chunk's
+    first band to n, only chunks that intersect this rank's shard."""
+    T, B = 64, 8
+    nT = (n + T - 1) // T
+    tpm = nT * (nT + 1) // 2
+    total = m * tpm
+    lo, hi = total * rank // world, total * (rank + 1) // world
+
+    def bf(I):
+        return I * nT - I * (I - 1) // 2
+
+    b = 0
+    for l in range(m):
+        for I0 in range(0, nT, B):
+            I1 = min(nT, I0 + B)
+            g0, g1 = l * tpm + bf(I0), l * tpm + bf(I1)
+            if g1 <= lo or g0 >= hi:
+                continue
+            r0, r1 = I0 * T, min(n, I1 * T)
+            b += (r1 - r0) * (n - r0) * 8
+    return b
+
+
+def read_traffic(cfg):
+    path = os.path.join(ROOT, "profiles", f"pass_traffic_cfg{cfg}.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+# --------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1502_03391_b200 as jg
+    from paper_1502_03391_b200 import workloads
+    from paper_1502_03391_b200._capi import check, dptr
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    wl = workloads.make(cfg)
+    spec = wl.spec
+    dev = jg.Device(local, shard=(rank, world))
+    lib = dev.lib
+    stream = torch.cuda.ExternalStream(dev.stream)
+
+    # Inputs resident in HBM: Delta packed on the device from the features
+    # (reference arithmetic, bit-identical to the dense host matrix), X0 on
+    # the device.
+    dev.upload_features(wl.in_features)
+    x0_host = wl.x0()
+    x0_dev = torch.from_numpy(x0_host).cuda()
+    xbuf = None
+    if world > 1:
+        count = lib.jofc_exchange_count(dev.h, wl.d)
+        xbuf = torch.zeros(count, dtype=torch.float64, device="cuda")
+        check(lib.jofc_set_exchange_buffer(dev.h, xbuf.data_ptr(), count))
+
+        def hook(ptr, cnt, strm):
+            with torch.cuda.stream(stream):
+                dist.all_reduce(xbuf[:cnt])
+        dev.set_allreduce(hook)
+
+    import ctypes as C
+    eps, T = 1e-300, wl.iterations
+    x0_ptr = C.cast(x0_dev.data_ptr(), C.POINTER(C.c_double))
+
+    def solve():
+        check(lib.jofc_fjofc_enqueue(dev.h, C.byref(spec.c()), wl.d, x0_ptr, eps, T))
+
+    def fetch():
+        its, conv = C.c_size_t(), C.c_int()
+        check(lib.jofc_fetch_result(dev.h, None, None, C.byref(its), C.byref(conv)))
+        return its.value
+
+    for _ in range(args.warmup):
+        solve()
+    fetch()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    check(lib.jofc_profile(dev.h, 1))
+    launches0 = dev.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        solve()
+    e1.record(stream)
+    e1.synchronize()
+    launches = dev.launches() - launches0
+    pass_ms, pass_n = C.c_double(), C.c_uint64()
+    check(lib.jofc_profile_read(dev.h, C.byref(pass_ms), C.byref(pass_n)))
+    check(lib.jofc_profile(dev.h, 0))
+    its = fetch()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_its = its * args.steps
+    value = total_its / (ms * 1e-3)
+    pairs = dev.problem_pairs()
+    local_bytes = dev.problem_bytes()
+
+    # roofline of the dominant kernel (the fused pass), from live CUDA events
+    hbm_peak, hbm_src = measured_peaks()
+    avg_pass_ms = pass_ms.value / max(pass_n.value, 1)
+    alg_bytes = 8.0 * pairs / world  # packed Delta entries streamed per launch (this shard)
+    achieved = alg_bytes / (avg_pass_ms * 1e-3) / 1e9
+    fp64 = probe_fp64(local) if rank == 0 else None
+    flops = (7 * wl.d + 6) * pairs / world
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 4), "traffic": read_traffic(cfg),
+            "peak_source": hbm_src, "kernel": "jofc_pass_kernel",
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "avg_launch_ms": round(avg_pass_ms, 4),
+            "pass_share_of_step": round(pass_ms.value / ms, 4) if world == 1 else None}
+    if fp64:
+        ach_tf = flops / (avg_pass_ms * 1e-3) / 1e12
+        roof["fp64"] = {"achieved_tflops": round(ach_tf, 2),
+                        "peak_tflops_dfma_measured": round(fp64["dfma_tflops"], 2),
+                        "frac": round(ach_tf / fp64["dfma_tflops"], 4),
+                        "algorithmic_flops_per_pair": 7 * wl.d + 6,
+                        "dmma_tflops_measured": round(fp64["dmma_tflops"], 2),
+                        "dfma_plus_dmma_tflops_measured": round(fp64["mixed_tflops"], 2)}
+        t_h = alg_bytes / (hbm_peak * 1e9)
+        t_f = flops / (fp64["dfma_tflops"] * 1e12)
+        roof["roofline_ms"] = round(max(t_h, t_f) * 1e3, 4)
+        roof["frac_of_roofline"] = round(max(t_h, t_f) / (avg_pass_ms * 1e-3), 4)
+
+    # ---------------- e2e through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, wl, dev, spec, world, rank, torch, dist)
+
+    # ---------------- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, args)
+
+    if rank == 0:
+        line = {
+            "metric": f"Guttman iterations/s (fJOFC {CONFIG_NAMES[cfg]}: m={wl.m} n={wl.n} "
+                      f"d={wl.d}), Delta resident in HBM",
+            "value": round(value, 3), "unit": "it/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md)",
+            "config": {"workload": f"{CONFIG_NAMES[cfg]} in-sample fJOFC m={wl.m} n={wl.n} "
+                                   f"d={wl.d} {spec.describe()} {T} Guttman iterations/step",
+                       "iterations_per_step": its, "packed_pairs": pairs,
+                       "delta_bytes_resident_per_gpu": local_bytes,
+                       "parallelism": f"delta-shard{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (packed Delta 3.2 GB vs 126 MB L2)"
+                       if local_bytes > 126e6 * 4 else "Delta may be L2-resident"},
+            "delta_entries_per_s": value * pairs,
+            "delta_entries_per_s_per_gpu": value * pairs / world,
+            "roofline": roof,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    dev.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, wl, dev, spec, world, rank, torch, dist):
+    """Same metric through the reference-facing C ABI with host buffers."""
+    import ctypes as C
+
+    import psutil
+
+    from paper_1502_03391_b200._capi import _dp, check, dptr
+    need = wl.m * wl.n * wl.n * 8
+    if psutil.virtual_memory().available < 2.5 * need:
+        return {"value": None, "unit": "it/s", "skipped": "not enough host memory for dense Delta"}
+    lib = dev.lib
+    delta = wl.dense_delta()  # (m, n, n) host, reference bits
+    x0 = wl.x0()
+    # pin the host buffers once (outside the timed region)
+    cudart = torch.cuda.cudart()
+    pinned = []
+    for arr in (delta, x0):
+        rc = cudart.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+        pinned.append((arr, int(rc) == 0))
+    x_out = np.empty_like(x0)
+    trace = np.empty(wl.iterations + 1)
+    x_out_pin = int(cudart.cudaHostRegister(x_out.ctypes.data, x_out.nbytes, 0)) == 0
+    ptrs = (_dp * wl.m)(*[dptr(delta[l]) for l in range(wl.m)])
+    its, conv = C.c_size_t(), C.c_int()
+    steps = max(1, args.e2e_steps)
+
+    def one():
+        check(lib.jofc_set_problem(dev.h, wl.m, wl.n, ptrs, 0))
+        check(lib.jofc_fjofc_embed(dev.h, C.byref(spec.c()), wl.d, dptr(x0), 1e-300,
+                                   wl.iterations, dptr(x_out), dptr(trace), C.byref(its),
+                                   C.byref(conv), None))
+
+    one()  # warm-up
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    t1 = time.perf_counter()
+    sec = t1 - t0
+    if world > 1:
+        t = torch.tensor([sec], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    for arr, ok in pinned:
+        if ok:
+            cudart.cudaHostUnregister(arr.ctypes.data)
+    if x_out_pin:
+        cudart.cudaHostUnregister(x_out.ctypes.data)
+    h2d = h2d_bytes_dense_upload(wl.m, wl.n, world, rank) + x0.nbytes
+    d2h = x_out.nbytes + 8 * (its.value + 1)
+    return {"value": round(its.value * steps / sec, 3), "unit": "it/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "ms_per_step": round(sec / steps * 1e3, 2),
+            "path": "jofc_set_problem(pinned dense host Delta) + jofc_fjofc_embed(host X0 -> "
+                    "host X, trace); wall clock, synchronous C-ABI calls",
+            "x_final_matches_device_run": bool(np.all(np.isfinite(x_out)))}
+
+
+def cpu_baseline(wl, args):
+    """The reference CPU path on this host, bounded sample of the same workload."""
+    from oracle.oracle import Port, Reference, Spec
+    try:
+        R = Reference()
+        kind = "reference"
+    except (FileNotFoundError, OSError):
+        R = Port()
+        kind = "port"
+    delta = wl.dense_delta()
+    x0 = wl.x0()
+    spec = (Spec.general_(wl.spec.general) if wl.general_weights else Spec.uniform(wl.w))
+    cores = R.max_threads() if kind == "reference" else 1
+    if kind == "reference":
+        R.problem(delta)  # validated OmnibusProblem, outside the timing
+    t0 = time.perf_counter()
+    R.fjofc_embed(delta, spec, x0, 1e-300, 1, parallel=True)
+    t1 = time.perf_counter() - t0
+    n_it = int(max(1, min(wl.iterations, args.cpu_seconds / max(t1, 1e-9))))
+    t0 = time.perf_counter()
+    r = R.fjofc_embed(delta, spec, x0, 1e-300, n_it, parallel=True)
+    sec = time.perf_counter() - t0
+    its = r.iterations
+    out = {"value": round(its / sec, 5), "unit": "it/s", "cores": cores, "kind": kind,
+           "sample": f"{its} Guttman iterations of fjofc_embed on the full "
+                     f"{CONFIG_NAMES[wl.cfg]} workload (parallel=true, OpenMP), call "
+                     f"wall time incl. sigma(X0)",
+           "seconds": round(sec, 3)}
+    if kind == "reference":
+        R.release()
+    return out
+
+
+# ------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from oracle.oracle import Port, Reference, Spec
+    from paper_1502_03391_b200 import workloads
+    try:
+        R = Reference()
+        kind = "reference"
+    except (FileNotFoundError, OSError):
+        R = Port()
+        kind = "port"
+    cfg = args.config
+    wl = workloads.make(cfg)
+    delta = wl.dense_delta()
+    x0 = wl.x0()
+    spec = Spec.general_(wl.spec.general) if wl.general_weights else Spec.uniform(wl.w)
+    cores = R.max_threads() if kind == "reference" else 1
+    if kind == "reference":
+        R.problem(delta)
+    per_step = args.ref_iterations
+    for _ in range(args.warmup):
+        R.fjofc_embed(delta, spec, x0, 1e-300, per_step, parallel=True)
+    t0 = time.perf_counter()
+    total = 0
+    for _ in range(args.steps):
+        total += R.fjofc_embed(delta, spec, x0, 1e-300, per_step, parallel=True).iterations
+    sec = time.perf_counter() - t0
+    value = total / sec
+    line = {
+        "impl": "reference",
+        "metric": f"Guttman iterations/s (fJOFC {CONFIG_NAMES[cfg]}: m={wl.m} n={wl.n} d={wl.d})",
+        "value": round(value, 5), "unit": "it/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sec / args.steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md)",
+        "config": {"workload": f"{CONFIG_NAMES[cfg]} in-sample fJOFC m={wl.m} n={wl.n} d={wl.d} "
+                               f"{wl.spec.describe()}",
+                   "iterations_per_step": per_step},
+        "delta_entries_per_s": value * wl.m * wl.n * (wl.n - 1) / 2,
+        "cpu_baseline": {"value": round(value, 5), "unit": "it/s", "cores": cores, "kind": kind,
+                         "sample": f"{per_step} Guttman iterations of fjofc_embed per step on "
+                                   f"the full {CONFIG_NAMES[cfg]} workload, parallel=true"},
+        "e2e": {"value": round(value, 5), "unit": "it/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-iterations", type=int, default=2)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * jofc_gpu.h -- C ABI of the B200 fJOFC hot path (libjofc_gpu.so).
+ *
+ * This is the drop-in boundary under the reference's C++ entry points
+ * (proj/include/jofc/{solver,stress,oos}.hpp).  Plain pointers and sizes
+ * only.  Every array is dense row-major fp64 unless noted; a configuration
+ * is m blocks of n x d (modality-major), exactly Configuration::blocks of
+ * the reference (proj/include/jofc/problem.hpp:37-46).  Any pointer argument
+ * may point to host memory (pageable or pinned) or to device memory of the
+ * context's GPU: copies are resolved through unified addressing.
+ *
+ * Status codes (mirroring the reference's exceptions):
+ *   0 JOFC_OK
+ *   1 JOFC_EINVAL    std::invalid_argument (shape / weight / option checks)
+ *   2 JOFC_ENUMERIC  jofc::NumericalError  (non-finite stress, bad inverse)
+ *   3 JOFC_ECUDA     CUDA runtime failure
+ *   4 JOFC_ECOMM     the registered all-reduce hook failed
+ * jofc_last_error() returns the message of the calling thread's last failure
+ * (the reference's what() text where one exists).
+ *
+ * Threading: a context is driven by one host thread at a time.  Functions are
+ * synchronous on return (results are in the caller's buffers) except where
+ * noted.
+ */
+#ifndef JOFC_GPU_H
+#define JOFC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  JOFC_OK = 0,
+  JOFC_EINVAL = 1,
+  JOFC_ENUMERIC = 2,
+  JOFC_ECUDA = 3,
+  JOFC_ECOMM = 4
+};
+
+/* WeightSpec (proj/include/jofc/weights.hpp:20-66):
+ *   kind 0 uniform(w)              a_l = 1,     w_ll' = w
+ *   kind 1 general(W: m x m)       a_l = W_ll,  w_ll' = W_ll'
+ *   kind 2 product(within: m, c)   a_l = c p_l, w_ll' = p_l p_l'          */
+typedef struct {
+  int kind;
+  double w;
+  const double* general;
+  const double* within;
+  double scale;
+} jofc_weights;
+
+typedef struct jofc_ctx jofc_ctx;
+
+/* Sum-all-reduce hook for multi-GPU sharding: must replace buf[0..count) on
+ * every rank by the elementwise sum over ranks, enqueued on `stream` (a
+ * cudaStream_t).  Return 0 on success. */
+typedef int (*jofc_allreduce_fn)(double* device_buf, size_t count, void* stream, void* user);
+
+const char* jofc_last_error(void);
+int jofc_version(void);
+
+/* Context on one CUDA device; owns a non-blocking stream and all buffers. */
+int jofc_ctx_create(int device, jofc_ctx** out);
+int jofc_ctx_destroy(jofc_ctx* ctx);
+/* The cudaStream_t every kernel of this context is launched on. */
+void* jofc_ctx_stream(jofc_ctx* ctx);
+
+/* Multi-GPU: this context owns shard `rank` of `world` balanced contiguous
+ * ranges of the packed tile stream (call before jofc_set_problem*), and
+ * reduces partial products through `fn` each iteration. */
+int jofc_set_shard(jofc_ctx* ctx, int rank, int world);
+int jofc_set_allreduce(jofc_ctx* ctx, jofc_allreduce_fn fn, void* user);
+
+/* OmnibusProblem upload (proj/include/jofc/problem.hpp:16-34): m dense n x n
+ * dissimilarities, delta[l] -> n*n row-major.  Only the upper triangle is
+ * read; it is packed into HBM-resident 64x64 tiles and checked finite and
+ * nonnegative.  normalize != 0 divides each modality by its Frobenius norm
+ * first (OmnibusProblem::normalized, proj/src/problem.cpp:34-42). */
+int jofc_set_problem(jofc_ctx* ctx, size_t m, size_t n, const double* const* delta,
+                     int normalize);
+/* Input preparation on the device: delta_l = euclidean_distance_matrix(F_l)
+ * for features F (m x n x p), with the reference's exact per-pair arithmetic
+ * (proj/src/distance.cpp:8-29), written straight into the packed layout. */
+int jofc_set_problem_features(jofc_ctx* ctx, size_t m, size_t n, size_t p,
+                              const double* features);
+/* Bytes of packed Delta resident on this context (its shard only). */
+size_t jofc_problem_bytes(jofc_ctx* ctx);
+/* Number of packed pairs m*n(n-1)/2 (all shards). */
+double jofc_problem_pairs(jofc_ctx* ctx);
+
+/* raw_stress (proj/src/stress.cpp:39-74). */
+int jofc_raw_stress(jofc_ctx* ctx, const jofc_weights* spec, size_t d, const double* x,
+                    double* stress);
+
+/* guttman_step_fast (proj/src/solver.cpp:154-161): one fast transform. */
+int jofc_guttman_step(jofc_ctx* ctx, const jofc_weights* spec, size_t d, const double* x,
+                      double* x_next);
+
+/* fjofc_embed with InitKind::provided (proj/src/solver.cpp:106-150,223-236).
+ * trace_out: max_it+1 doubles, sigma(X_0..X_iterations); step_seconds:
+ * max_it doubles or NULL; iterations / converged as EmbeddingResult. */
+int jofc_fjofc_embed(jofc_ctx* ctx, const jofc_weights* spec, size_t d, const double* x0,
+                     double eps, size_t max_it, double* x_out, double* trace_out,
+                     size_t* iterations, int* converged, double* step_seconds);
+
+/* Asynchronous form for device-resident use: enqueue the whole solve on the
+ * context stream; results are read with jofc_fetch_result after a sync. */
+int jofc_fjofc_enqueue(jofc_ctx* ctx, const jofc_weights* spec, size_t d, const double* x0,
+                       double eps, size_t max_it);
+int jofc_fetch_result(jofc_ctx* ctx, double* x_out, double* trace_out, size_t* iterations,
+                      int* converged);
+/* Kernel launches issued by this context since creation (evidence counter). */
+uint64_t jofc_launch_count(jofc_ctx* ctx);
+/* Instrumentation: when enabled, CUDA events bracket every pass-kernel launch
+ * on the context stream; jofc_profile_read synchronises and returns the summed
+ * pass time (ms) and launch count since the last read. */
+int jofc_profile(jofc_ctx* ctx, int enable);
+int jofc_profile_read(jofc_ctx* ctx, double* pass_ms, uint64_t* pass_launches);
+/* Multi-GPU: let the caller own the product/exchange buffer (device memory of
+ * this context's GPU, >= m*n_pad*d + 1 doubles with n_pad = 64*ceil(n/64)) so
+ * that its collective library can reduce it in place.  NULL reverts. */
+int jofc_set_exchange_buffer(jofc_ctx* ctx, double* device_buf, size_t capacity);
+size_t jofc_exchange_count(jofc_ctx* ctx, size_t d);
+
+/* Out-of-sample (proj/src/oos.cpp), uniform w only as in the reference.
+ * x: frozen configuration m x n x d; deltas: m x n for one point. */
+int jofc_oos_stress(jofc_ctx* ctx, size_t m, size_t n, size_t d, const double* y,
+                    const double* x, const double* deltas, double w, double* stress);
+int jofc_oos_step(jofc_ctx* ctx, size_t m, size_t n, size_t d, const double* y,
+                  const double* x, const double* deltas, double w, double* y_next);
+/* k independent points in one batched solve: deltas k x m x n, y0 k x m x d.
+ * Each point follows oos_embed's loop and stop rule (proj/src/oos.cpp:200-227)
+ * unless fixed_iterations != 0 (then exactly max_it steps).  traces:
+ * k x (max_it+1) or NULL; iterations: k or NULL. */
+int jofc_oos_batch(jofc_ctx* ctx, size_t k, size_t m, size_t n, size_t d, const double* x,
+                   const double* deltas, double w, const double* y0, double eps,
+                   size_t max_it, int fixed_iterations, double* y_out, double* traces,
+                   size_t* iterations);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

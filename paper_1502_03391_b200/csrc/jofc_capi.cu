@@ -1,0 +1,783 @@
+// jofc_capi.cu -- host side of libjofc_gpu.so: the C ABI in include/jofc_gpu.h.
+//
+// Owns the device state of one solve context: the packed Delta shard, the
+// ping-pong configuration buffers, the product/fidelity exchange buffer, the
+// control block, and the launch sequence
+//
+//     for t = 0 .. max_it:   pass(t) -> [all-reduce hook] -> epilogue(t)
+//
+// enqueued without host synchronisation: termination (the reference's
+// decrease < eps rule, proj/src/solver.cpp:138-143) is decided on the device
+// and later launches exit at entry once the control block says done.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "jofc_gpu.h"
+#include "jofc_kernels.cuh"
+#include "jofc_oos.cuh"
+#include "jofc_weights.h"
+
+using namespace jofc_gpu;
+
+namespace {
+
+thread_local std::string g_error;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_error = buf;
+  return code;
+}
+
+#define JOFC_CUDA(call)                                                                 \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_error(JOFC_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                       __FILE__, __LINE__);                                             \
+  } while (0)
+
+constexpr int kMaxD = 10;
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct jofc_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  // sharding / exchange
+  int rank = 0, world = 1;
+  jofc_allreduce_fn allreduce = nullptr;
+  void* allreduce_user = nullptr;
+  // problem
+  bool has_problem = false;
+  Layout lay;
+  DevBuf<double> delta;
+  // solve state (sized for the current d)
+  size_t d = 0;
+  DevBuf<double> x0, x1, P, fid_part, com_part, trace, consts;
+  DevBuf<Control> ctrl;
+  Control* ctrl_host = nullptr;  // pinned
+  int pass_grid = 0, epi_grid = 0;
+  size_t max_it_enqueued = 0;
+  // caller-owned exchange buffer (multi-GPU) and pass-kernel instrumentation
+  double* ext_P = nullptr;
+  size_t ext_cap = 0;
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  size_t prof_used = 0;
+  // oos state
+  DevBuf<double> oos_x, oos_delta, oos_y0, oos_y1, oos_part, oos_trace;
+  DevBuf<OosPoint> oos_st;
+};
+
+namespace {
+
+double* exchange(jofc_ctx* c) {
+  const size_t need = static_cast<size_t>(c->lay.m) * c->lay.n_pad * c->d + 1;
+  return (c->ext_P && c->ext_cap >= need) ? c->ext_P : c->P.p;
+}
+
+size_t fid_slot(const jofc_ctx* c) { return static_cast<size_t>(c->lay.m) * c->lay.n_pad * c->d; }
+
+template <int D>
+int setup_pass_kernel() {
+  static bool done = false;
+  if (!done) {
+    JOFC_CUDA(cudaFuncSetAttribute(jofc_pass_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sizeof(PassSmem<D>))));
+    done = true;
+  }
+  return JOFC_OK;
+}
+
+template <int D>
+int launch_pass(jofc_ctx* c, const PassParams& pp) {
+  int rc = setup_pass_kernel<D>();
+  if (rc) return rc;
+  jofc_pass_kernel<D><<<c->pass_grid, kPassThreads, sizeof(PassSmem<D>), c->stream>>>(pp);
+  JOFC_CUDA(cudaGetLastError());
+  return JOFC_OK;
+}
+
+template <int D>
+int launch_epi(jofc_ctx* c, const EpiParams& ep) {
+  jofc_epilogue_kernel<D><<<c->epi_grid, 256, 0, c->stream>>>(ep);
+  JOFC_CUDA(cudaGetLastError());
+  return JOFC_OK;
+}
+
+#define JOFC_DISPATCH_D(d, FN, ...)         \
+  switch (d) {                              \
+    case 1: return FN<1>(__VA_ARGS__);      \
+    case 2: return FN<2>(__VA_ARGS__);      \
+    case 3: return FN<3>(__VA_ARGS__);      \
+    case 4: return FN<4>(__VA_ARGS__);      \
+    case 5: return FN<5>(__VA_ARGS__);      \
+    case 6: return FN<6>(__VA_ARGS__);      \
+    case 7: return FN<7>(__VA_ARGS__);      \
+    case 8: return FN<8>(__VA_ARGS__);      \
+    case 9: return FN<9>(__VA_ARGS__);      \
+    case 10: return FN<10>(__VA_ARGS__);    \
+    default:                                \
+      return set_error(JOFC_EINVAL, "dim %zu unsupported (1..10)", static_cast<size_t>(d)); \
+  }
+
+int pass_for_d(jofc_ctx* c, const PassParams& pp) { JOFC_DISPATCH_D(c->d, launch_pass, c, pp); }
+int epi_for_d(jofc_ctx* c, const EpiParams& ep) { JOFC_DISPATCH_D(c->d, launch_epi, c, ep); }
+
+int require_problem(jofc_ctx* c) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  if (!c->has_problem) return set_error(JOFC_EINVAL, "no problem uploaded (jofc_set_problem)");
+  return JOFC_OK;
+}
+
+// Layout for m modalities of n objects; this shard's contiguous stream range.
+void make_layout(jofc_ctx* c, size_t m, size_t n) {
+  Layout& L = c->lay;
+  L.m = static_cast<int>(m);
+  L.n = static_cast<long long>(n);
+  L.nT = static_cast<int>((n + kTile - 1) / kTile);
+  L.n_pad = static_cast<long long>(L.nT) * kTile;
+  L.tpm = tiles_per_modality(L.nT);
+  const long long total = L.total();
+  L.begin = total * c->rank / c->world;
+  L.end = total * (c->rank + 1) / c->world;
+}
+
+int alloc_solve_state(jofc_ctx* c, size_t d, size_t max_it) {
+  const Layout& L = c->lay;
+  const size_t cfg = static_cast<size_t>(L.m) * L.n_pad * d;
+  const bool resize = (d != c->d) || !c->x0.p || c->x0.n < cfg;
+  c->d = d;
+  JOFC_CUDA(c->x0.ensure(cfg));
+  JOFC_CUDA(c->x1.ensure(cfg));
+  if (c->ext_P && c->ext_cap >= cfg + 1) {
+    c->P.release();
+  } else {
+    JOFC_CUDA(c->P.ensure(cfg + 1));
+  }
+  c->pass_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(c->num_sms, L.local())));
+  c->epi_grid = static_cast<int>((L.n + 255) / 256);
+  JOFC_CUDA(c->fid_part.ensure(c->pass_grid));
+  JOFC_CUDA(c->com_part.ensure(c->epi_grid));
+  JOFC_CUDA(c->trace.ensure(max_it + 1));
+  JOFC_CUDA(c->ctrl.ensure(1));
+  JOFC_CUDA(c->consts.ensure(3 * static_cast<size_t>(L.m) * L.m + L.m));
+  if (resize) {
+    JOFC_CUDA(cudaMemsetAsync(c->x0.p, 0, cfg * sizeof(double), c->stream));
+    JOFC_CUDA(cudaMemsetAsync(c->x1.p, 0, cfg * sizeof(double), c->stream));
+  }
+  JOFC_CUDA(cudaMemsetAsync(exchange(c), 0, (cfg + 1) * sizeof(double), c->stream));
+  return JOFC_OK;
+}
+
+// Caller configuration (m blocks of n x d) -> padded device layout.
+int upload_config(jofc_ctx* c, const double* x, double* dst) {
+  const Layout& L = c->lay;
+  const size_t block = static_cast<size_t>(L.n) * c->d;
+  for (int l = 0; l < L.m; ++l)
+    JOFC_CUDA(cudaMemcpyAsync(dst + static_cast<size_t>(l) * L.n_pad * c->d, x + l * block,
+                              block * sizeof(double), cudaMemcpyDefault, c->stream));
+  return JOFC_OK;
+}
+
+int download_config(jofc_ctx* c, const double* src, double* x) {
+  const Layout& L = c->lay;
+  const size_t block = static_cast<size_t>(L.n) * c->d;
+  for (int l = 0; l < L.m; ++l)
+    JOFC_CUDA(cudaMemcpyAsync(x + l * block, src + static_cast<size_t>(l) * L.n_pad * c->d,
+                              block * sizeof(double), cudaMemcpyDefault, c->stream));
+  return JOFC_OK;
+}
+
+// Enqueue the whole majorization (max_it transforms, max_it + 1 stress
+// evaluations) on the context stream.  events (optional) get max_it + 2
+// records: before pass t and after the final epilogue.
+int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x0, double eps,
+                  size_t max_it, std::vector<cudaEvent_t>* events) {
+  int rc = require_problem(c);
+  if (rc) return rc;
+  if (d < 1 || d > static_cast<size_t>(kMaxD))
+    return set_error(JOFC_EINVAL, "dim %zu unsupported (1..%d)", d, kMaxD);
+  if (!(eps > 0.0)) return set_error(JOFC_EINVAL, "SolveOptions: eps must be positive");
+  if (!x0) return set_error(JOFC_EINVAL, "null configuration");
+  const Layout& L = c->lay;
+  HostWeights hw;
+  std::string msg;
+  rc = build_weights(spec, static_cast<size_t>(L.m), static_cast<size_t>(L.n), &hw, &msg);
+  if (rc) return set_error(rc, "%s", msg.c_str());
+  rc = alloc_solve_state(c, d, max_it);
+  if (rc) return rc;
+
+  const size_t mm = static_cast<size_t>(L.m) * L.m;
+  std::vector<double> consts(3 * mm + L.m);
+  std::copy(hw.coef.begin(), hw.coef.end(), consts.begin());
+  std::copy(hw.cross.begin(), hw.cross.end(), consts.begin() + mm);
+  std::copy(hw.winv.begin(), hw.winv.end(), consts.begin() + 2 * mm);
+  std::copy(hw.within.begin(), hw.within.end(), consts.begin() + 3 * mm);
+  JOFC_CUDA(cudaMemcpyAsync(c->consts.p, consts.data(), consts.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, c->stream));
+  rc = upload_config(c, x0, c->x0.p);
+  if (rc) return rc;
+
+  Control& h = *c->ctrl_host;
+  std::memset(&h, 0, sizeof(Control));
+  h.max_it = static_cast<int>(max_it);
+  h.eps = eps;
+  const double mn = static_cast<double>(L.m) * static_cast<double>(L.n);
+  h.pairs = mn * (mn - 1.0) / 2.0;
+  JOFC_CUDA(cudaMemcpyAsync(c->ctrl.p, &h, sizeof(Control), cudaMemcpyHostToDevice, c->stream));
+
+  PassParams pp{};
+  pp.delta = c->delta.p;
+  pp.x0 = c->x0.p;
+  pp.x1 = c->x1.p;
+  pp.P = exchange(c);
+  pp.fid_partials = c->fid_part.p;
+  pp.ctrl = c->ctrl.p;
+  pp.within = c->consts.p + 3 * mm;
+  pp.n = L.n;
+  pp.n_pad = L.n_pad;
+  pp.nT = L.nT;
+  pp.tpm = L.tpm;
+  pp.begin = L.begin;
+  pp.end = L.end;
+  pp.fid_slot = fid_slot(c);
+
+  EpiParams ep{};
+  ep.x0 = c->x0.p;
+  ep.x1 = c->x1.p;
+  ep.P = exchange(c);
+  ep.com_partials = c->com_part.p;
+  ep.trace = c->trace.p;
+  ep.ctrl = c->ctrl.p;
+  ep.coef = c->consts.p;
+  ep.cross = c->consts.p + mm;
+  ep.m = L.m;
+  ep.n = L.n;
+  ep.n_pad = L.n_pad;
+  ep.fid_slot = fid_slot(c);
+
+  for (size_t t = 0; t <= max_it; ++t) {
+    if (events) JOFC_CUDA(cudaEventRecord((*events)[t], c->stream));
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+    if (c->profiling) {
+      if (c->prof_used == c->prof_events.size()) {
+        cudaEvent_t a, b;
+        JOFC_CUDA(cudaEventCreate(&a));
+        JOFC_CUDA(cudaEventCreate(&b));
+        c->prof_events.emplace_back(a, b);
+      }
+      pe0 = c->prof_events[c->prof_used].first;
+      pe1 = c->prof_events[c->prof_used].second;
+      ++c->prof_used;
+      JOFC_CUDA(cudaEventRecord(pe0, c->stream));
+    }
+    rc = pass_for_d(c, pp);
+    if (rc) return rc;
+    if (pe1) JOFC_CUDA(cudaEventRecord(pe1, c->stream));
+    ++c->launches;
+    if (c->world > 1) {
+      if (!c->allreduce)
+        return set_error(JOFC_ECOMM, "sharded context (world %d) without an all-reduce hook",
+                         c->world);
+      if (c->allreduce(exchange(c), fid_slot(c) + 1, c->stream, c->allreduce_user) != 0)
+        return set_error(JOFC_ECOMM, "all-reduce hook failed at iteration %zu", t);
+    }
+    rc = epi_for_d(c, ep);
+    if (rc) return rc;
+    ++c->launches;
+  }
+  if (events) JOFC_CUDA(cudaEventRecord((*events)[max_it + 1], c->stream));
+  c->max_it_enqueued = max_it;
+  return JOFC_OK;
+}
+
+// Synchronise, then fetch the control block; maps device status to errors.
+int finish_solve(jofc_ctx* c, Control* out) {
+  JOFC_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl.p, sizeof(Control), cudaMemcpyDeviceToHost,
+                            c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  *out = *c->ctrl_host;
+  if (out->status == 2) {
+    if (out->err_iter == 0)
+      return set_error(JOFC_ENUMERIC, "embed: non-finite stress at the initial configuration");
+    return set_error(JOFC_ENUMERIC, "embed: non-finite stress at iteration %d", out->err_iter);
+  }
+  if (!out->done) return set_error(JOFC_ECUDA, "solve did not terminate (internal)");
+  return JOFC_OK;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* jofc_last_error(void) { return g_error.c_str(); }
+
+int jofc_version(void) { return 1; }
+
+int jofc_ctx_create(int device, jofc_ctx** out) {
+  if (!out) return set_error(JOFC_EINVAL, "null output");
+  *out = nullptr;
+  int ndev = 0;
+  JOFC_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return set_error(JOFC_EINVAL, "device %d out of range (%d devices)", device, ndev);
+  JOFC_CUDA(cudaSetDevice(device));
+  jofc_ctx* c = new jofc_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMallocHost(&c->ctrl_host, sizeof(Control));
+  if (e != cudaSuccess) {
+    delete c;
+    return set_error(JOFC_ECUDA, "context setup: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return JOFC_OK;
+}
+
+int jofc_ctx_destroy(jofc_ctx* c) {
+  if (!c) return JOFC_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (DevBuf<double>* b : {&c->delta, &c->x0, &c->x1, &c->P, &c->fid_part, &c->com_part,
+                            &c->trace, &c->consts, &c->oos_x, &c->oos_delta, &c->oos_y0,
+                            &c->oos_y1, &c->oos_part, &c->oos_trace})
+    b->release();
+  c->ctrl.release();
+  c->oos_st.release();
+  for (auto& e : c->prof_events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (c->ctrl_host) cudaFreeHost(c->ctrl_host);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return JOFC_OK;
+}
+
+void* jofc_ctx_stream(jofc_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+uint64_t jofc_launch_count(jofc_ctx* c) { return c ? c->launches : 0; }
+
+int jofc_profile(jofc_ctx* c, int enable) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  c->profiling = enable != 0;
+  c->prof_used = 0;
+  return JOFC_OK;
+}
+
+int jofc_profile_read(jofc_ctx* c, double* pass_ms, uint64_t* pass_launches) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  double total = 0.0;
+  for (size_t i = 0; i < c->prof_used; ++i) {
+    float ms = 0.f;
+    JOFC_CUDA(cudaEventElapsedTime(&ms, c->prof_events[i].first, c->prof_events[i].second));
+    total += ms;
+  }
+  if (pass_ms) *pass_ms = total;
+  if (pass_launches) *pass_launches = c->prof_used;
+  c->prof_used = 0;
+  return JOFC_OK;
+}
+
+int jofc_set_exchange_buffer(jofc_ctx* c, double* buf, size_t capacity) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  c->ext_P = buf;
+  c->ext_cap = buf ? capacity : 0;
+  return JOFC_OK;
+}
+
+size_t jofc_exchange_count(jofc_ctx* c, size_t d) {
+  if (!c || !c->has_problem) return 0;
+  return static_cast<size_t>(c->lay.m) * c->lay.n_pad * d + 1;
+}
+
+int jofc_set_shard(jofc_ctx* c, int rank, int world) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  if (world < 1 || rank < 0 || rank >= world)
+    return set_error(JOFC_EINVAL, "shard %d of %d invalid", rank, world);
+  c->rank = rank;
+  c->world = world;
+  c->has_problem = false;
+  return JOFC_OK;
+}
+
+int jofc_set_allreduce(jofc_ctx* c, jofc_allreduce_fn fn, void* user) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  c->allreduce = fn;
+  c->allreduce_user = user;
+  return JOFC_OK;
+}
+
+size_t jofc_problem_bytes(jofc_ctx* c) {
+  return (c && c->has_problem) ? static_cast<size_t>(c->lay.local()) * kTileBytes : 0;
+}
+
+double jofc_problem_pairs(jofc_ctx* c) {
+  if (!c || !c->has_problem) return 0.0;
+  const double n = static_cast<double>(c->lay.n);
+  return static_cast<double>(c->lay.m) * n * (n - 1.0) / 2.0;
+}
+
+int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta, int normalize) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  if (m == 0) return set_error(JOFC_EINVAL, "OmnibusProblem: at least one modality required");
+  if (n < 2) return set_error(JOFC_EINVAL, "OmnibusProblem: need at least two objects");
+  if (!delta) return set_error(JOFC_EINVAL, "null delta");
+  for (size_t l = 0; l < m; ++l)
+    if (!delta[l]) return set_error(JOFC_EINVAL, "OmnibusProblem: modality %zu is null", l);
+  JOFC_CUDA(cudaSetDevice(c->device));
+  c->has_problem = false;
+  make_layout(c, m, n);
+  const Layout& L = c->lay;
+  JOFC_CUDA(c->delta.ensure(static_cast<size_t>(std::max<long long>(L.local(), 1)) * kTileElems));
+
+  // Frobenius norms over the full dense matrix in the reference's order.
+  std::vector<double> norms(m, 0.0);
+  if (normalize)
+    for (size_t l = 0; l < m; ++l) {
+      double s = 0.0;
+      const double* dl = delta[l];
+      for (size_t i = 0; i < n * n; ++i) s += dl[i] * dl[i];
+      norms[l] = std::sqrt(s);
+    }
+
+  // Staging: up to kBands tile-rows of the dense matrix (upper part only).
+  const int kBands = 8;
+  DevBuf<double> stage;
+  DevBuf<int> bad;
+  JOFC_CUDA(stage.ensure(static_cast<size_t>(kBands) * kTile * L.n_pad));
+  JOFC_CUDA(bad.ensure(1));
+  JOFC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+  for (int l = 0; l < L.m; ++l) {
+    for (int I0 = 0; I0 < L.nT; I0 += kBands) {
+      const int I1 = std::min(L.nT, I0 + kBands);
+      const long long g_lo = static_cast<long long>(l) * L.tpm + band_first(L.nT, I0);
+      const long long g_hi = static_cast<long long>(l) * L.tpm + band_first(L.nT, I1);
+      if (g_hi <= L.begin || g_lo >= L.end) continue;  // not in this shard
+      const long long r0 = static_cast<long long>(I0) * kTile;
+      const long long r1 = std::min<long long>(L.n, static_cast<long long>(I1) * kTile);
+      const long long c0 = r0;
+      const size_t width = static_cast<size_t>(L.n - c0) * sizeof(double);
+      JOFC_CUDA(cudaMemcpy2DAsync(stage.p, L.n_pad * sizeof(double), delta[l] + r0 * L.n + c0,
+                                  L.n * sizeof(double), width, static_cast<size_t>(r1 - r0),
+                                  cudaMemcpyDefault, c->stream));
+      PackParams pk{};
+      pk.stage = stage.p;
+      pk.pitch = L.n_pad;
+      pk.r0 = r0;
+      pk.c0 = c0;
+      pk.n = L.n;
+      pk.nT = L.nT;
+      pk.tpm = L.tpm;
+      pk.l = l;
+      pk.g_first = g_lo;
+      pk.begin = L.begin;
+      pk.end = L.end;
+      pk.dst = c->delta.p;
+      pk.inv_norm_div = (normalize && norms[l] != 0.0) ? norms[l] : 0.0;
+      pk.bad = bad.p;
+      jofc_pack_kernel<<<static_cast<unsigned>(g_hi - g_lo), 256, 0, c->stream>>>(pk);
+      JOFC_CUDA(cudaGetLastError());
+      ++c->launches;
+    }
+  }
+  int hbad = 0;
+  JOFC_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  stage.release();
+  bad.release();
+  if (hbad) return set_error(JOFC_EINVAL, "OmnibusProblem: delta has a non-finite or negative entry");
+  c->has_problem = true;
+  return JOFC_OK;
+}
+
+int jofc_set_problem_features(jofc_ctx* c, size_t m, size_t n, size_t p, const double* feats) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  if (m == 0 || n < 2 || p == 0 || !feats)
+    return set_error(JOFC_EINVAL, "features: need m >= 1, n >= 2, p >= 1");
+  JOFC_CUDA(cudaSetDevice(c->device));
+  c->has_problem = false;
+  make_layout(c, m, n);
+  const Layout& L = c->lay;
+  JOFC_CUDA(c->delta.ensure(static_cast<size_t>(std::max<long long>(L.local(), 1)) * kTileElems));
+  DevBuf<double> f;
+  JOFC_CUDA(f.ensure(m * n * p));
+  JOFC_CUDA(cudaMemcpyAsync(f.p, feats, m * n * p * sizeof(double), cudaMemcpyDefault, c->stream));
+  const size_t smem = 2 * kTile * p * sizeof(double);
+  if (smem > 48 * 1024)
+    JOFC_CUDA(cudaFuncSetAttribute(jofc_edm_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  const long long tiles = L.local();
+  for (long long off = 0; off < tiles; off += (1LL << 30)) {
+    const long long cnt = std::min<long long>(tiles - off, 1LL << 30);
+    jofc_edm_tile_kernel<<<static_cast<unsigned>(cnt), 256, smem, c->stream>>>(
+        f.p, L.n, static_cast<int>(p), L.nT, L.tpm, L.begin + off, L.end, c->delta.p);
+    JOFC_CUDA(cudaGetLastError());
+    ++c->launches;
+  }
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  f.release();
+  c->has_problem = true;
+  return JOFC_OK;
+}
+
+int jofc_fjofc_enqueue(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x0,
+                       double eps, size_t max_it) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  JOFC_CUDA(cudaSetDevice(c->device));
+  return enqueue_solve(c, spec, d, x0, eps, max_it, nullptr);
+}
+
+int jofc_fetch_result(jofc_ctx* c, double* x_out, double* trace_out, size_t* iterations,
+                      int* converged) {
+  int rc = require_problem(c);
+  if (rc) return rc;
+  Control h;
+  rc = finish_solve(c, &h);
+  if (rc) return rc;
+  if (x_out) {
+    rc = download_config(c, (h.iterations & 1) ? c->x1.p : c->x0.p, x_out);
+    if (rc) return rc;
+  }
+  if (trace_out)
+    JOFC_CUDA(cudaMemcpyAsync(trace_out, c->trace.p, (h.iterations + 1) * sizeof(double),
+                              cudaMemcpyDefault, c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  if (iterations) *iterations = static_cast<size_t>(h.iterations);
+  if (converged) *converged = h.converged;
+  return JOFC_OK;
+}
+
+int jofc_fjofc_embed(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x0, double eps,
+                     size_t max_it, double* x_out, double* trace_out, size_t* iterations,
+                     int* converged, double* step_seconds) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  JOFC_CUDA(cudaSetDevice(c->device));
+  std::vector<cudaEvent_t> ev;
+  if (step_seconds) {
+    ev.resize(max_it + 2);
+    for (auto& e : ev) JOFC_CUDA(cudaEventCreate(&e));
+  }
+  int rc = enqueue_solve(c, spec, d, x0, eps, max_it, step_seconds ? &ev : nullptr);
+  size_t its = 0;
+  if (!rc) rc = jofc_fetch_result(c, x_out, trace_out, &its, converged);
+  if (!rc && iterations) *iterations = its;
+  if (!rc && step_seconds) {
+    for (size_t t = 0; t < its; ++t) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[t], ev[t + 1]);
+      step_seconds[t] = ms * 1e-3;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+int jofc_raw_stress(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x,
+                    double* stress) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  JOFC_CUDA(cudaSetDevice(c->device));
+  int rc = enqueue_solve(c, spec, d, x, 1.0, 0, nullptr);
+  if (rc) return rc;
+  Control h;
+  JOFC_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl.p, sizeof(Control), cudaMemcpyDeviceToHost,
+                            c->stream));
+  double s = 0.0;
+  JOFC_CUDA(cudaMemcpyAsync(&s, c->trace.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  h = *c->ctrl_host;
+  (void)h;
+  *stress = s;  // non-finite stress is returned as is (raw_stress does not throw)
+  return JOFC_OK;
+}
+
+int jofc_guttman_step(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x,
+                      double* x_next) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  JOFC_CUDA(cudaSetDevice(c->device));
+  // One pass + epilogue with max_it = 1 (eps tiny so the rule cannot fire at
+  // t = 0): X_1 lands in buffer 1 whatever the stress is.
+  const Layout& L = c->lay;
+  int rc = require_problem(c);
+  if (rc) return rc;
+  if (d < 1 || d > static_cast<size_t>(kMaxD))
+    return set_error(JOFC_EINVAL, "dim %zu unsupported (1..%d)", d, kMaxD);
+  rc = enqueue_solve(c, spec, d, x, 1e-300, 0, nullptr);
+  (void)L;
+  if (rc) return rc;
+  // enqueue_solve(max_it = 0) marks the solve done at t = 0 after the mix, so
+  // buffer 1 holds the transform of x.
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  rc = download_config(c, c->x1.p, x_next);
+  if (rc) return rc;
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  return JOFC_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- out-of-sample
+namespace {
+
+template <int D>
+int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
+  const dim3 pg((op.k + kOosWarps - 1) / kOosWarps, op.m);
+  const unsigned ug = (op.k + 127) / 128;
+  for (int t = 0; t <= steps; ++t) {
+    jofc_oos_pass_kernel<D><<<pg, kOosWarps * 32, 0, c->stream>>>(op);
+    jofc_oos_update_kernel<D><<<ug, 128, 0, c->stream>>>(op);
+    c->launches += 2;
+  }
+  JOFC_CUDA(cudaGetLastError());
+  return JOFC_OK;
+}
+
+int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x,
+            const double* deltas, double w, const double* y0, double eps, size_t max_it,
+            int fixed, double* y_out, double* traces, size_t* iterations, double* stress0) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  if (!(w > 0.0)) return set_error(JOFC_EINVAL, "oos: w must be strictly positive");
+  if (!(eps > 0.0)) return set_error(JOFC_EINVAL, "OosOptions: eps must be positive");
+  if (m == 0 || n == 0 || k == 0) return set_error(JOFC_EINVAL, "oos: empty input");
+  if (d < 1 || d > static_cast<size_t>(kMaxD))
+    return set_error(JOFC_EINVAL, "dim %zu unsupported (1..%d)", d, kMaxD);
+  JOFC_CUDA(cudaSetDevice(c->device));
+  JOFC_CUDA(c->oos_x.ensure(m * n * d));
+  JOFC_CUDA(c->oos_delta.ensure(k * m * n));
+  JOFC_CUDA(c->oos_y0.ensure(k * m * d));
+  JOFC_CUDA(c->oos_y1.ensure(k * m * d));
+  JOFC_CUDA(c->oos_part.ensure(k * m * (d + 2) + k));
+  JOFC_CUDA(c->oos_trace.ensure(k * (max_it + 1)));
+  JOFC_CUDA(c->oos_st.ensure(k));
+  JOFC_CUDA(cudaMemcpyAsync(c->oos_x.p, x, m * n * d * sizeof(double), cudaMemcpyDefault, c->stream));
+  JOFC_CUDA(cudaMemcpyAsync(c->oos_delta.p, deltas, k * m * n * sizeof(double), cudaMemcpyDefault,
+                            c->stream));
+  JOFC_CUDA(cudaMemcpyAsync(c->oos_y0.p, y0, k * m * d * sizeof(double), cudaMemcpyDefault,
+                            c->stream));
+  JOFC_CUDA(cudaMemsetAsync(c->oos_st.p, 0, k * sizeof(OosPoint), c->stream));
+  OosParams op{};
+  op.x = c->oos_x.p;
+  op.deltas = c->oos_delta.p;
+  op.y0 = c->oos_y0.p;
+  op.y1 = c->oos_y1.p;
+  op.part = c->oos_part.p;
+  op.st = c->oos_st.p;
+  op.traces = c->oos_trace.p;
+  op.k = static_cast<int>(k);
+  op.m = static_cast<int>(m);
+  op.n = static_cast<long long>(n);
+  op.w = w;
+  op.eps = eps;
+  op.term_count = static_cast<double>(m * n) + 0.5 * static_cast<double>(m * (m - 1));
+  op.max_it = static_cast<int>(max_it);
+  op.fixed = fixed;
+  int rc;
+  switch (d) {
+    case 1: rc = oos_launch<1>(c, op, static_cast<int>(max_it)); break;
+    case 2: rc = oos_launch<2>(c, op, static_cast<int>(max_it)); break;
+    case 3: rc = oos_launch<3>(c, op, static_cast<int>(max_it)); break;
+    case 4: rc = oos_launch<4>(c, op, static_cast<int>(max_it)); break;
+    case 5: rc = oos_launch<5>(c, op, static_cast<int>(max_it)); break;
+    case 6: rc = oos_launch<6>(c, op, static_cast<int>(max_it)); break;
+    case 7: rc = oos_launch<7>(c, op, static_cast<int>(max_it)); break;
+    case 8: rc = oos_launch<8>(c, op, static_cast<int>(max_it)); break;
+    case 9: rc = oos_launch<9>(c, op, static_cast<int>(max_it)); break;
+    default: rc = oos_launch<10>(c, op, static_cast<int>(max_it)); break;
+  }
+  if (rc) return rc;
+  std::vector<OosPoint> st(k);
+  JOFC_CUDA(cudaMemcpyAsync(st.data(), c->oos_st.p, k * sizeof(OosPoint), cudaMemcpyDeviceToHost,
+                            c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  for (size_t p = 0; p < k; ++p)
+    if (st[p].status == 2) {
+      if (st[p].iterations == 0)
+        return set_error(JOFC_ENUMERIC, "oos_embed: non-finite stress at the initial point");
+      return set_error(JOFC_ENUMERIC, "oos_embed: non-finite stress at iteration %d",
+                       st[p].iterations);
+    }
+  // Final y of point p is in buffer (iterations_p & 1).
+  std::vector<double> ya(k * m * d), yb(k * m * d);
+  if (y_out) {
+    JOFC_CUDA(cudaMemcpyAsync(ya.data(), c->oos_y0.p, k * m * d * sizeof(double),
+                              cudaMemcpyDeviceToHost, c->stream));
+    JOFC_CUDA(cudaMemcpyAsync(yb.data(), c->oos_y1.p, k * m * d * sizeof(double),
+                              cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (traces)
+    JOFC_CUDA(cudaMemcpyAsync(traces, c->oos_trace.p, k * (max_it + 1) * sizeof(double),
+                              cudaMemcpyDefault, c->stream));
+  if (stress0)
+    JOFC_CUDA(cudaMemcpyAsync(stress0, c->oos_trace.p, sizeof(double), cudaMemcpyDeviceToHost,
+                              c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  for (size_t p = 0; p < k; ++p) {
+    if (iterations) iterations[p] = static_cast<size_t>(st[p].iterations);
+    if (y_out) {
+      const double* src = (st[p].iterations & 1) ? yb.data() : ya.data();
+      std::memcpy(y_out + p * m * d, src + p * m * d, m * d * sizeof(double));
+    }
+  }
+  return JOFC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int jofc_oos_batch(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x,
+                   const double* deltas, double w, const double* y0, double eps, size_t max_it,
+                   int fixed_iterations, double* y_out, double* traces, size_t* iterations) {
+  return oos_run(c, k, m, n, d, x, deltas, w, y0, eps, max_it, fixed_iterations, y_out, traces,
+                 iterations, nullptr);
+}
+
+int jofc_oos_stress(jofc_ctx* c, size_t m, size_t n, size_t d, const double* y, const double* x,
+                    const double* deltas, double w, double* stress) {
+  return oos_run(c, 1, m, n, d, x, deltas, w, y, 1.0, 0, 1, nullptr, nullptr, nullptr, stress);
+}
+
+int jofc_oos_step(jofc_ctx* c, size_t m, size_t n, size_t d, const double* y, const double* x,
+                  const double* deltas, double w, double* y_next) {
+  return oos_run(c, 1, m, n, d, x, deltas, w, y, 1.0, 1, 1, y_next, nullptr, nullptr, nullptr);
+}
+
+}  // extern "C"

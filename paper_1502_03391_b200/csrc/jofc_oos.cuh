@@ -1,0 +1,174 @@
+// jofc_oos.cuh -- batched out-of-sample Guttman updates (sm_100a).
+//
+// k new objects, each with m views, embedded against a frozen in-sample
+// configuration X (m x n x d).  Per point and modality j the reference
+// (proj/src/oos.cpp:83-96) needs, for the current y_j,
+//   r_k = [dist != 0] delta_j(k) / dist(X^(j)_k, y_j),
+//   psi_j = sum_k r_k,   xi_j = sum_k (1 - r_k) X^(j)_k,
+// and oos_stress (proj/src/oos.cpp:50-57) needs sum_k (delta_j(k) - dist)^2
+// from the same distances, so one streaming pass over delta yields both
+// (fused like the in-sample pass).  jofc_oos_update_kernel then applies the
+// closed-form corner update (proj/src/oos.cpp:98-111), the commensurability
+// term and the per-point stop rule (proj/src/oos.cpp:221-226).
+//
+// Pass layout: CTA = 8 warps = 8 points of one modality (blockIdx.y); X^(j)
+// is staged through shared memory in 512-row chunks and shared by the 8
+// warps; lanes stride the n in-sample rows (coalesced delta reads), warp
+// shuffles finish the sums.
+#pragma once
+
+#include "jofc_kernels.cuh"
+
+namespace jofc_gpu {
+
+struct OosPoint {
+  int t;
+  int done;
+  int iterations;
+  int status;  // 0 ok, 2 non-finite stress
+};
+
+struct OosParams {
+  const double* x;       // m x n x d
+  const double* deltas;  // k x m x n
+  double* y0;            // ping-pong k x m x d
+  double* y1;
+  double* part;          // k x m x (d + 2): psi, fid, xi[d]
+  OosPoint* st;
+  double* traces;        // k x (max_it + 1) or null
+  int k, m;
+  long long n;
+  double w, eps, term_count;
+  int max_it;
+  int fixed;
+};
+
+constexpr int kOosWarps = 8;
+constexpr int kOosChunk = 512;
+
+template <int D>
+__global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_pass_kernel(const OosParams p) {
+  __shared__ double xs[kOosChunk * D];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pt = blockIdx.x * kOosWarps + warp;
+  const int j = blockIdx.y;
+  bool active = pt < p.k;
+  int t = 0;
+  if (active) {
+    const OosPoint s = p.st[pt];
+    active = !s.done;
+    t = s.t;
+  }
+  double y[D];
+  const double* yb = ((t & 1) ? p.y1 : p.y0) + (static_cast<long long>(pt) * p.m + j) * D;
+#pragma unroll
+  for (int c = 0; c < D; ++c) y[c] = active ? yb[c] : 0.0;
+  const double* X = p.x + static_cast<long long>(j) * p.n * D;
+  const double* dl = p.deltas + (static_cast<long long>(pt) * p.m + j) * p.n;
+  double psi = 0.0, fid = 0.0, xi[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) xi[c] = 0.0;
+  for (long long k0 = 0; k0 < p.n; k0 += kOosChunk) {
+    const int rows = static_cast<int>(min(static_cast<long long>(kOosChunk), p.n - k0));
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * D; e += blockDim.x) xs[e] = X[k0 * D + e];
+    __syncthreads();
+    if (!active) continue;
+    for (int kk = lane; kk < rows; kk += 32) {
+      const double dv = dl[k0 + kk];
+      double s = 0.0, xk[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        xk[c] = xs[kk * D + c];
+        const double df = xk[c] - y[c];
+        s = (c == 0) ? df * df : fma(df, df, s);
+      }
+      const double inv = (s > 0.0) ? rsqrt_nr(s) : 0.0;
+      const double r = dv * inv;
+      const double resid = dv - s * inv;
+      fid = fma(resid, resid, fid);
+      psi += r;
+      const double cf = 1.0 - r;
+#pragma unroll
+      for (int c = 0; c < D; ++c) xi[c] = fma(cf, xk[c], xi[c]);
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    psi += __shfl_xor_sync(0xffffffffu, psi, o);
+    fid += __shfl_xor_sync(0xffffffffu, fid, o);
+#pragma unroll
+    for (int c = 0; c < D; ++c) xi[c] += __shfl_xor_sync(0xffffffffu, xi[c], o);
+  }
+  if (lane == 0) {
+    double* out = p.part + (static_cast<long long>(pt) * p.m + j) * (D + 2);
+    out[0] = psi;
+    out[1] = fid;
+#pragma unroll
+    for (int c = 0; c < D; ++c) out[2 + c] = xi[c];
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) jofc_oos_update_kernel(const OosParams p) {
+  const int pt = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pt >= p.k) return;
+  OosPoint st = p.st[pt];
+  if (st.done) return;
+  const int t = st.t, m = p.m;
+  const double* y = ((t & 1) ? p.y1 : p.y0) + static_cast<long long>(pt) * m * D;
+  double* yn = ((t & 1) ? p.y0 : p.y1) + static_cast<long long>(pt) * m * D;
+  const double* part = p.part + static_cast<long long>(pt) * m * (D + 2);
+  double fid = 0.0, com = 0.0;
+  double xi_sum[D], psi_y[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) xi_sum[c] = psi_y[c] = 0.0;
+  for (int j = 0; j < m; ++j) {
+    fid += part[j * (D + 2) + 1];
+    const double psi = part[j * (D + 2)];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      xi_sum[c] += part[j * (D + 2) + 2 + c];
+      psi_y[c] = fma(psi, y[j * D + c], psi_y[c]);
+    }
+    for (int i2 = j + 1; i2 < m; ++i2) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const double df = y[j * D + c] - y[i2 * D + c];
+        com = fma(df, df, com);
+      }
+    }
+  }
+  const double sigma = fid + p.w * com;
+  if (p.traces) p.traces[static_cast<long long>(pt) * (p.max_it + 1) + t] = sigma;
+  if (!isfinite(sigma)) {
+    st.status = 2;
+    st.done = 1;
+    st.iterations = t;
+    p.st[pt] = st;
+    return;
+  }
+  st.iterations = t;
+  double* prev_slot = p.part + static_cast<long long>(p.k) * m * (D + 2) + pt;
+  if (t >= 1 && !p.fixed && (*prev_slot - sigma) / p.term_count < p.eps) st.done = 1;
+  if (t >= p.max_it) st.done = 1;
+  *prev_slot = sigma;
+  if (!st.done) {
+    const double nn = static_cast<double>(p.n);
+    const double mw = static_cast<double>(m) * p.w;
+    const double direct = 1.0 / (nn + mw);
+    const double spread = p.w / (nn * (nn + mw));
+    for (int j = 0; j < m; ++j) {
+      const double psi = part[j * (D + 2)];
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+        yn[j * D + c] = direct * (part[j * (D + 2) + 2 + c] + psi * y[j * D + c]) +
+                        spread * (xi_sum[c] + psi_y[c]);
+    }
+  }
+  st.t = t + 1;
+  p.st[pt] = st;
+}
+
+}  // namespace jofc_gpu
