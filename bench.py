@@ -103,26 +103,29 @@ class ClockSampler:
 
 
 def h2d_bytes_dense_upload(m, n, world, rank):
-    """Bytes jofc_set_problem copies: 8-band row chunks, columns from the chunk's
-    first band to n, only chunks that intersect this rank's shard."""
-    T, B = 64, 8
-    nT = (n + T - 1) // T
-    tpm = nT * (nT + 1) // 2
-    total = m * tpm
+    """Bytes jofc_set_problem copies: chunks of 4 row blocks (512 rows), columns
+    from the chunk's first row to n, only chunks that meet this rank's shard
+    (layout: paper_1502_03391_b200/csrc/jofc_layout.h)."""
+    R, C, K = 128, 64, 4
+    nT = (n + C - 1) // C
+    nB = (nT + 1) // 2
+
+    def rf(B):
+        return B * nT - B * (B - 1)
+
+    bpm = rf(nB)
+    total = m * bpm
     lo, hi = total * rank // world, total * (rank + 1) // world
-
-    def bf(I):
-        return I * nT - I * (I - 1) // 2
-
     b = 0
     for l in range(m):
-        for I0 in range(0, nT, B):
-            I1 = min(nT, I0 + B)
-            g0, g1 = l * tpm + bf(I0), l * tpm + bf(I1)
+        for B0 in range(0, nB, K):
+            B1 = min(nB, B0 + K)
+            g0, g1 = l * bpm + rf(B0), l * bpm + rf(B1)
             if g1 <= lo or g0 >= hi:
                 continue
-            r0, r1 = I0 * T, min(n, I1 * T)
-            b += (r1 - r0) * (n - r0) * 8
+            r0, r1 = B0 * R, min(n, B1 * R)
+            if r1 > r0:
+                b += (r1 - r0) * (n - r0) * 8
     return b
 
 
@@ -269,7 +272,7 @@ def run_ours(args):
                        "iterations_per_step": its, "packed_pairs": pairs,
                        "delta_bytes_resident_per_gpu": local_bytes,
                        "parallelism": f"delta-shard{world}" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (packed Delta 3.2 GB vs 126 MB L2)"
+                       "l2": "inputs larger than L2 (packed Delta %.2f GB vs 126 MB L2)" % (local_bytes / 1e9)
                        if local_bytes > 126e6 * 4 else "Delta may be L2-resident"},
             "delta_entries_per_s": value * pairs,
             "delta_entries_per_s_per_gpu": value * pairs / world,

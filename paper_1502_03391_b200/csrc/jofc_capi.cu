@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,24 +113,39 @@ double* exchange(jofc_ctx* c) {
 
 size_t fid_slot(const jofc_ctx* c) { return static_cast<size_t>(c->lay.m) * c->lay.n_pad * c->d; }
 
-template <int D>
-int setup_pass_kernel() {
-  static bool done = false;
-  if (!done) {
-    JOFC_CUDA(cudaFuncSetAttribute(jofc_pass_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int D, int VAR>
+int launch_pass_var(jofc_ctx* c, const PassParams& pp) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    JOFC_CUDA(cudaFuncSetAttribute(jofc_pass_kernel<D, VAR>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(sizeof(PassSmem<D>))));
-    done = true;
+    attr_done = true;
   }
+  jofc_pass_kernel<D, VAR><<<c->pass_grid, kPassThreads, sizeof(PassSmem<D>), c->stream>>>(pp);
+  JOFC_CUDA(cudaGetLastError());
   return JOFC_OK;
+}
+
+int pass_variant() {
+  static int v = [] {
+    const char* e = getenv("JOFC_VARIANT");  // kernel-variant experiments
+    return e ? atoi(e) : 0;
+  }();
+  return v;
 }
 
 template <int D>
 int launch_pass(jofc_ctx* c, const PassParams& pp) {
-  int rc = setup_pass_kernel<D>();
-  if (rc) return rc;
-  jofc_pass_kernel<D><<<c->pass_grid, kPassThreads, sizeof(PassSmem<D>), c->stream>>>(pp);
-  JOFC_CUDA(cudaGetLastError());
-  return JOFC_OK;
+  if (D == 5 || D == 3) {
+    switch (pass_variant()) {
+      case 1: return launch_pass_var<D, 1>(c, pp);
+      case 2: return launch_pass_var<D, 2>(c, pp);
+      case 3: return launch_pass_var<D, 3>(c, pp);
+      default: break;
+    }
+  }
+  return launch_pass_var<D, 0>(c, pp);
 }
 
 template <int D>
@@ -169,9 +185,10 @@ void make_layout(jofc_ctx* c, size_t m, size_t n) {
   Layout& L = c->lay;
   L.m = static_cast<int>(m);
   L.n = static_cast<long long>(n);
-  L.nT = static_cast<int>((n + kTile - 1) / kTile);
-  L.n_pad = static_cast<long long>(L.nT) * kTile;
-  L.tpm = tiles_per_modality(L.nT);
+  L.nT = static_cast<int>((n + kCols - 1) / kCols);
+  L.nB = (L.nT + 1) / 2;
+  L.n_pad = static_cast<long long>(L.nB) * kRows;
+  L.bpm = blocks_per_modality(L.nT);
   const long long total = L.total();
   L.begin = total * c->rank / c->world;
   L.end = total * (c->rank + 1) / c->world;
@@ -272,10 +289,14 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   pp.n = L.n;
   pp.n_pad = L.n_pad;
   pp.nT = L.nT;
-  pp.tpm = L.tpm;
+  pp.bpm = L.bpm;
   pp.begin = L.begin;
   pp.end = L.end;
   pp.fid_slot = fid_slot(c);
+  {
+    const char* dg = getenv("JOFC_DIAG");  // experiments only; results are wrong when set
+    pp.diag = dg ? atoi(dg) : 0;
+  }
 
   EpiParams ep{};
   ep.x0 = c->x0.p;
@@ -447,7 +468,7 @@ int jofc_set_allreduce(jofc_ctx* c, jofc_allreduce_fn fn, void* user) {
 }
 
 size_t jofc_problem_bytes(jofc_ctx* c) {
-  return (c && c->has_problem) ? static_cast<size_t>(c->lay.local()) * kTileBytes : 0;
+  return (c && c->has_problem) ? static_cast<size_t>(c->lay.local()) * kBlockBytes : 0;
 }
 
 double jofc_problem_pairs(jofc_ctx* c) {
@@ -467,7 +488,7 @@ int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta
   c->has_problem = false;
   make_layout(c, m, n);
   const Layout& L = c->lay;
-  JOFC_CUDA(c->delta.ensure(static_cast<size_t>(std::max<long long>(L.local(), 1)) * kTileElems));
+  JOFC_CUDA(c->delta.ensure(static_cast<size_t>(std::max<long long>(L.local(), 1)) * kBlockElems));
 
   // Frobenius norms over the full dense matrix in the reference's order.
   std::vector<double> norms(m, 0.0);
@@ -479,26 +500,29 @@ int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta
       norms[l] = std::sqrt(s);
     }
 
-  // Staging: up to kBands tile-rows of the dense matrix (upper part only).
-  const int kBands = 8;
+  // Staging: up to kChunk row blocks (128 rows each) of the dense matrix,
+  // columns from the chunk's first row onwards (the upper part only).
+  const int kChunk = 4;
   DevBuf<double> stage;
   DevBuf<int> bad;
-  JOFC_CUDA(stage.ensure(static_cast<size_t>(kBands) * kTile * L.n_pad));
+  JOFC_CUDA(stage.ensure(static_cast<size_t>(kChunk) * kRows * L.n_pad));
   JOFC_CUDA(bad.ensure(1));
   JOFC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
   for (int l = 0; l < L.m; ++l) {
-    for (int I0 = 0; I0 < L.nT; I0 += kBands) {
-      const int I1 = std::min(L.nT, I0 + kBands);
-      const long long g_lo = static_cast<long long>(l) * L.tpm + band_first(L.nT, I0);
-      const long long g_hi = static_cast<long long>(l) * L.tpm + band_first(L.nT, I1);
+    for (int B0 = 0; B0 < L.nB; B0 += kChunk) {
+      const int B1 = std::min(L.nB, B0 + kChunk);
+      const long long g_lo = static_cast<long long>(l) * L.bpm + row_first(L.nT, B0);
+      const long long g_hi = static_cast<long long>(l) * L.bpm + row_first(L.nT, B1);
       if (g_hi <= L.begin || g_lo >= L.end) continue;  // not in this shard
-      const long long r0 = static_cast<long long>(I0) * kTile;
-      const long long r1 = std::min<long long>(L.n, static_cast<long long>(I1) * kTile);
+      const long long r0 = static_cast<long long>(B0) * kRows;
+      const long long r1 = std::min<long long>(L.n, static_cast<long long>(B1) * kRows);
       const long long c0 = r0;
-      const size_t width = static_cast<size_t>(L.n - c0) * sizeof(double);
-      JOFC_CUDA(cudaMemcpy2DAsync(stage.p, L.n_pad * sizeof(double), delta[l] + r0 * L.n + c0,
-                                  L.n * sizeof(double), width, static_cast<size_t>(r1 - r0),
-                                  cudaMemcpyDefault, c->stream));
+      if (r1 > r0 && c0 < L.n) {
+        const size_t width = static_cast<size_t>(L.n - c0) * sizeof(double);
+        JOFC_CUDA(cudaMemcpy2DAsync(stage.p, L.n_pad * sizeof(double), delta[l] + r0 * L.n + c0,
+                                    L.n * sizeof(double), width, static_cast<size_t>(r1 - r0),
+                                    cudaMemcpyDefault, c->stream));
+      }
       PackParams pk{};
       pk.stage = stage.p;
       pk.pitch = L.n_pad;
@@ -506,13 +530,12 @@ int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta
       pk.c0 = c0;
       pk.n = L.n;
       pk.nT = L.nT;
-      pk.tpm = L.tpm;
-      pk.l = l;
+      pk.bpm = L.bpm;
       pk.g_first = g_lo;
       pk.begin = L.begin;
       pk.end = L.end;
       pk.dst = c->delta.p;
-      pk.inv_norm_div = (normalize && norms[l] != 0.0) ? norms[l] : 0.0;
+      pk.norm = (normalize && norms[l] != 0.0) ? norms[l] : 0.0;
       pk.bad = bad.p;
       jofc_pack_kernel<<<static_cast<unsigned>(g_hi - g_lo), 256, 0, c->stream>>>(pk);
       JOFC_CUDA(cudaGetLastError());
@@ -537,19 +560,20 @@ int jofc_set_problem_features(jofc_ctx* c, size_t m, size_t n, size_t p, const d
   c->has_problem = false;
   make_layout(c, m, n);
   const Layout& L = c->lay;
-  JOFC_CUDA(c->delta.ensure(static_cast<size_t>(std::max<long long>(L.local(), 1)) * kTileElems));
+  JOFC_CUDA(c->delta.ensure(static_cast<size_t>(std::max<long long>(L.local(), 1)) * kBlockElems));
   DevBuf<double> f;
   JOFC_CUDA(f.ensure(m * n * p));
   JOFC_CUDA(cudaMemcpyAsync(f.p, feats, m * n * p * sizeof(double), cudaMemcpyDefault, c->stream));
-  const size_t smem = 2 * kTile * p * sizeof(double);
+  const size_t smem = (kRows + kCols) * p * sizeof(double);
   if (smem > 48 * 1024)
-    JOFC_CUDA(cudaFuncSetAttribute(jofc_edm_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    JOFC_CUDA(cudaFuncSetAttribute(jofc_edm_block_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-  const long long tiles = L.local();
-  for (long long off = 0; off < tiles; off += (1LL << 30)) {
-    const long long cnt = std::min<long long>(tiles - off, 1LL << 30);
-    jofc_edm_tile_kernel<<<static_cast<unsigned>(cnt), 256, smem, c->stream>>>(
-        f.p, L.n, static_cast<int>(p), L.nT, L.tpm, L.begin + off, L.end, c->delta.p);
+  const long long blocks = L.local();
+  for (long long off = 0; off < blocks; off += (1LL << 30)) {
+    const long long cnt = std::min<long long>(blocks - off, 1LL << 30);
+    jofc_edm_block_kernel<<<static_cast<unsigned>(cnt), 256, smem, c->stream>>>(
+        f.p, L.n, static_cast<int>(p), L.nT, L.bpm, L.begin + off, L.end, c->delta.p);
     JOFC_CUDA(cudaGetLastError());
     ++c->launches;
   }

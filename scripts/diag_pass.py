@@ -1,0 +1,51 @@
+"""Time the fused pass kernel alone under experiment switches (JOFC_DIAG).
+
+python scripts/diag_pass.py [--config 3] [--modes 0,1,2,3]
+Modes (results are WRONG for modes != 0; timing experiments only):
+  0 normal, 1 no column RED, 2 column plain stores, 3 no column reduction.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_1502_03391_b200 as jg  # noqa: E402
+from paper_1502_03391_b200 import workloads  # noqa: E402
+from paper_1502_03391_b200._capi import check, dptr  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--modes", default="0,1,2,3")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--n", type=int, default=None)
+    a = ap.parse_args()
+    wl = workloads.make(a.config, n=a.n)
+    dev = jg.Device(0)
+    dev.upload_features(wl.in_features)
+    x0 = wl.x0()
+    lib = dev.lib
+    pairs = dev.problem_pairs()
+    for mode in [int(x) for x in a.modes.split(",")]:
+        os.environ["JOFC_DIAG"] = str(mode)
+        # single-pass solves (max_it = 0): every launch does the full pass even
+        # when the experiment corrupts the iterate
+        for rep in range(2):
+            check(lib.jofc_profile(dev.h, 1))
+            for _ in range(a.iters):
+                check(lib.jofc_fjofc_enqueue(dev.h, C.byref(wl.spec.c()), wl.d, dptr(x0), 1e-300,
+                                             0))
+            ms, n = C.c_double(), C.c_uint64()
+            check(lib.jofc_profile_read(dev.h, C.byref(ms), C.byref(n)))
+        avg = ms.value / n.value
+        print(f"cfg{a.config} mode {mode}: pass {avg:.4f} ms  {8 * pairs / avg / 1e6:.1f} GB/s "
+              f"({n.value} launches)", flush=True)
+    os.environ.pop("JOFC_DIAG")
+
+
+if __name__ == "__main__":
+    main()

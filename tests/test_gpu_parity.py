@@ -17,6 +17,17 @@ pytestmark = pytest.mark.gpu
 X_TOL = 1e-8
 S_TOL = 1e-10
 STEP_TOL = 1e-12
+# Stress entries are compared at S_TOL relative; when a tiny-n case fits the
+# data almost exactly (sigma_t ~ 1e-10 sigma_0) the relative error of such a
+# near-zero sum is meaningless, so an absolute floor of 1e-13 sigma_0 applies
+# (rounding of the individual residual terms is ~1e-16 of their scale).
+ABS_FLOOR = 1e-13
+
+
+def trace_close(got, ref):
+    s0 = abs(ref[0])
+    k = min(len(got), len(ref))
+    return all(abs(a - b) <= S_TOL * abs(b) + ABS_FLOOR * s0 for a, b in zip(got[:k], ref[:k]))
 
 
 @pytest.fixture(scope="module")
@@ -57,10 +68,8 @@ def test_golden_solves(dev, golden):
                               init=jg.InitKind.provided, init_config=x)
         r = jg.fjofc_embed(prob, spec, opt, device=dev)
         ref_tr = golden[p + "solve_trace"]
-        k = min(len(r.stress_trace), len(ref_tr))
-        assert k >= 2
-        for a, b in zip(r.stress_trace[:k], ref_tr[:k]):
-            assert rel(a, b) < S_TOL, p
+        assert min(len(r.stress_trace), len(ref_tr)) >= 2
+        assert trace_close(r.stress_trace, ref_tr), p
         if r.iterations == int(golden[p + "solve_iters"]):
             assert rel_fro(r.config, golden[p + "solve_x"]) < X_TOL, p
 
@@ -232,9 +241,7 @@ def test_oos_golden(dev, golden):
         assert rel(jg.oos_stress(y, x, dl, w, device=dev), float(golden[p + "stress"])) < STEP_TOL
         assert rel_fro(jg.oos_step_fast(y, x, dl, w, device=dev), golden[p + "step"]) < STEP_TOL
         e = jg.oos_embed(x, dl, w, jg.OosOptions(1e-6, 300), int(golden[p + "seed"]), device=dev)
-        ref_tr = golden[p + "embed_trace"]
-        k = min(len(e.stress_trace), len(ref_tr))
-        assert max(rel(a, b) for a, b in zip(e.stress_trace[:k], ref_tr[:k])) < S_TOL
+        assert trace_close(e.stress_trace, golden[p + "embed_trace"]), p
         assert rel_fro(e.y, golden[p + "embed_y"]) < 1e-7, p
 
 
