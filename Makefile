@@ -16,7 +16,7 @@ GPU_HDR := $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/jofc_gpu.h include/jofc
 DROPIN_SRC := $(wildcard $(CSRC)/dropin/*.cpp)
 DROPIN_HDR := $(wildcard include/jofc/*.hpp)
 
-all: $(PKG)/libjofc_gpu.so $(PKG)/libjofc_probe.so oracle
+all: $(PKG)/libjofc_gpu.so $(PKG)/libjofc.so $(PKG)/libjofc_probe.so oracle build/dropin_parity
 
 $(PKG)/libjofc_probe.so: $(CSRC)/probe.cu
 	$(NVCC) $(NVFLAGS) -shared -o $@ $<
@@ -30,6 +30,13 @@ $(PKG)/libjofc.so: $(DROPIN_SRC) $(DROPIN_HDR) $(PKG)/libjofc_gpu.so
 
 oracle:
 	$(MAKE) -C oracle all
+
+# C++ parity suite of the drop-in API (run by tests/test_dropin_cpp.py on a GPU)
+build/dropin_parity: tests/cpp/dropin_parity.cpp $(PKG)/libjofc.so oracle/jofc_oracle.c
+	@mkdir -p build
+	$(MAKE) -C oracle all
+	$(CXX) -std=c++20 -O2 -Iinclude -Ioracle -o $@ $< -L$(PKG) -ljofc -ljofc_gpu \
+	    -Loracle -ljofc_oracle -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,'$$ORIGIN/../oracle'
 
 ref:
 	$(MAKE) -C oracle ref

@@ -1,0 +1,75 @@
+"""Multi-GPU plumbing for the sharded Guttman loop (one process per GPU).
+
+Each rank owns a balanced contiguous range of the packed Delta block stream
+(jofc_set_shard); every iteration the partial product P = B(X)X (m*n_pad*d
+doubles) and the partial fidelity ride in one exchange buffer that must be
+sum-all-reduced before the epilogue (W^-1 mix, stress, stop rule) runs
+redundantly on every rank.  The buffer is a torch tensor handed to the C ABI
+(jofc_set_exchange_buffer) so torch.distributed/NCCL reduces it in place on
+the context's stream.
+"""
+from __future__ import annotations
+
+import threading
+
+from ._capi import check
+
+
+class _CudaView:
+    """__cuda_array_interface__ wrapper: raw device pointer -> torch tensor."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 2,
+                                         "strides": None}
+
+
+def cuda_view(ptr, count, device):
+    import torch
+    return torch.as_tensor(_CudaView(ptr, count), device=device)
+
+
+def attach_nccl(dev, d, group=None):
+    """Give `dev` (a paper_1502_03391_b200.Device with a shard set) a torch-owned
+    exchange buffer and an all-reduce hook over torch.distributed."""
+    import torch
+    import torch.distributed as dist
+    count = dev.lib.jofc_exchange_count(dev.h, d)
+    buf = torch.zeros(count, dtype=torch.float64, device=f"cuda:{dev.device}")
+    check(dev.lib.jofc_set_exchange_buffer(dev.h, buf.data_ptr(), count))
+    stream = torch.cuda.ExternalStream(dev.stream, device=f"cuda:{dev.device}")
+
+    def hook(ptr, cnt, strm):
+        with torch.cuda.stream(stream):
+            dist.all_reduce(buf[:cnt], group=group)
+    dev.set_allreduce(hook)
+    dev._xbuf = buf
+    return buf
+
+
+class ThreadGroup:
+    """Single-process stand-in for a W-rank group: W contexts, each driven by
+    its own host thread, reduce their exchange buffers on the host side (the
+    device never waits on another context's kernels).  Test use only."""
+
+    def __init__(self, world):
+        self.world = world
+        self.bar = threading.Barrier(world)
+        self.views = [None] * world
+
+    def hook_for(self, rank, device):
+        import torch
+
+        def hook(ptr, count, stream):
+            torch.cuda.ExternalStream(stream, device=device).synchronize()
+            self.views[rank] = cuda_view(ptr, count, device)
+            self.bar.wait()
+            if rank == 0:
+                total = self.views[0].clone()
+                for v in self.views[1:]:
+                    total += v
+                for v in self.views:
+                    v.copy_(total)
+                torch.cuda.synchronize(device)
+            self.bar.wait()
+        return hook

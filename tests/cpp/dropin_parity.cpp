@@ -1,0 +1,276 @@
+// C++ parity suite for the drop-in jofc:: API (libjofc.so over the CUDA path),
+// written the way the reference's own suites are (proj/tests/test_embed_core.cpp,
+// proj/tests/test_oos.cpp): seeded random problems, checks against an oracle.
+// The oracle is the C restatement (oracle/jofc_oracle.c), itself pinned
+// bit-for-bit to the reference by tests/test_oracle.py.  Exit code = failures.
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "jofc/linalg.hpp"
+#include "jofc/oos.hpp"
+#include "jofc/rng.hpp"
+#include "jofc/solver.hpp"
+#include "jofc/stress.hpp"
+#include "jofc/weights.hpp"
+#include "jofc_oracle.h"
+
+using namespace jofc;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                              \
+  do {                                                                           \
+    ++g_checks;                                                                  \
+    if (!(cond)) {                                                               \
+      ++g_fail;                                                                  \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);      \
+    }                                                                            \
+  } while (0)
+
+template <class E, class F>
+bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------- helpers
+static DenseMatrix random_matrix(Rng& rng, std::size_t r, std::size_t c, double scale = 1.0) {
+  DenseMatrix m(r, c);
+  for (std::size_t i = 0; i < m.size(); ++i) m.data()[i] = scale * rng.normal();
+  return m;
+}
+
+static DenseMatrix edm(const DenseMatrix& x) {
+  DenseMatrix out(x.rows(), x.rows());
+  jo_euclidean_distance_matrix(x.rows(), x.cols(), x.data(), out.data());
+  return out;
+}
+
+static OmnibusProblem random_problem(Rng& rng, std::size_t n, std::size_t m, std::size_t dim) {
+  std::vector<DenseMatrix> mods;
+  for (std::size_t l = 0; l < m; ++l) mods.push_back(edm(random_matrix(rng, n, dim, 2.0)));
+  return OmnibusProblem(std::move(mods));
+}
+
+static Configuration random_config(Rng& rng, std::size_t n, std::size_t m, std::size_t d,
+                                   double scale = 1.0) {
+  Configuration c;
+  for (std::size_t l = 0; l < m; ++l) c.blocks.push_back(random_matrix(rng, n, d, scale));
+  return c;
+}
+
+static std::vector<WeightSpec> families(std::size_t m, double w) {
+  std::vector<WeightSpec> out{WeightSpec::uniform(w)};
+  DenseMatrix g(m, m);
+  for (std::size_t i = 0; i < m; ++i)
+    for (std::size_t j = 0; j < m; ++j)
+      g(i, j) = (i == j) ? w * (1.0 + 0.1 * i) : w * (1.0 + 0.25 * std::abs(double(i) - double(j)));
+  out.push_back(WeightSpec::general(g));
+  std::vector<double> within(m);
+  for (std::size_t i = 0; i < m; ++i) within[i] = w * (1.0 + 0.5 * i);
+  out.push_back(WeightSpec::product(within, 1.5));
+  return out;
+}
+
+struct OracleSpec {
+  jo_weights w{};
+  std::vector<double> g, p;
+  explicit OracleSpec(const WeightSpec& s) {
+    if (s.kind() == WeightSpec::Kind::uniform) {
+      w.kind = 0;
+      w.w = s.uniform_w();
+    } else if (s.kind() == WeightSpec::Kind::general_symmetric) {
+      w.kind = 1;
+      g.assign(s.general_matrix().data(), s.general_matrix().data() + s.general_matrix().size());
+      w.general = g.data();
+    } else {
+      w.kind = 2;
+      p = s.product_within();
+      w.within = p.data();
+      w.scale = s.fidelity_scale();
+    }
+  }
+};
+
+static std::vector<double> flat(const Configuration& c) {
+  std::vector<double> v;
+  for (const auto& b : c.blocks) v.insert(v.end(), b.data(), b.data() + b.size());
+  return v;
+}
+
+static std::vector<double> flat(const OmnibusProblem& p) {
+  std::vector<double> v;
+  for (std::size_t l = 0; l < p.modality_count(); ++l)
+    v.insert(v.end(), p.modality(l).data(), p.modality(l).data() + p.modality(l).size());
+  return v;
+}
+
+static double rel_fro(const std::vector<double>& a, const std::vector<double>& b) {
+  double num = 0.0, den = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    num += (a[i] - b[i]) * (a[i] - b[i]);
+    den += b[i] * b[i];
+  }
+  return std::sqrt(num) / (den > 0 ? std::sqrt(den) : 1.0);
+}
+
+static double rel(double a, double b) { return std::abs(a - b) / std::max(std::abs(b), 1e-300); }
+
+// ---------------------------------------------------------------- tests
+static void fast_step_grid() {
+  // proj/tests/test_embed_core.cpp:170-183 grid, against the oracle
+  Rng rng(38);
+  for (std::size_t m : {1, 2, 3})
+    for (std::size_t n : {3, 5, 8, 70})
+      for (std::size_t d : {1, 2, 3})
+        for (double w : {0.5, 1.0, 10.0})
+          for (const WeightSpec& spec : families(m, w)) {
+            const OmnibusProblem problem = random_problem(rng, n, m, d);
+            const Configuration x = random_config(rng, n, m, d);
+            const Configuration step = guttman_step_fast(x, problem, spec);
+            const OracleSpec os(spec);
+            const auto delta = flat(problem);
+            const auto xf = flat(x);
+            std::vector<double> ref(xf.size());
+            jo_guttman_step_fast(m, n, d, delta.data(), &os.w, xf.data(), ref.data());
+            CHECK(rel_fro(flat(step), ref) < 1e-12);
+            double s_ref = 0.0;
+            jo_raw_stress(m, n, d, delta.data(), &os.w, xf.data(), &s_ref);
+            CHECK(rel(raw_stress(x, problem, spec), s_ref) < 1e-12);
+          }
+}
+
+static void solve_trajectory() {
+  // proj/tests/test_embed_core.cpp:310-329 style: same iterates as the oracle
+  Rng rng(47);
+  for (std::size_t m : {1, 2, 3}) {
+    const std::size_t n = 90, d = 2;
+    const OmnibusProblem problem = random_problem(rng, n, m, d);
+    const Configuration start = random_config(rng, n, m, d);
+    for (const WeightSpec& spec : families(m, 0.8)) {
+      SolveOptions opt;
+      opt.dim = d;
+      opt.max_iterations = 30;
+      opt.eps = 1e-300;
+      opt.init = InitKind::provided;
+      opt.init_config = start;
+      const EmbeddingResult r = fjofc_embed(problem, spec, opt);
+      const OracleSpec os(spec);
+      const auto delta = flat(problem);
+      const auto x0 = flat(start);
+      std::vector<double> xr(x0.size()), tr(31);
+      std::size_t its = 0;
+      int conv = 0;
+      jo_fjofc_embed(m, n, d, delta.data(), &os.w, x0.data(), 1e-300, 30, 0, xr.data(), tr.data(),
+                     &its, &conv);
+      CHECK(r.iterations == its);
+      CHECK(rel_fro(flat(r.config), xr) < 1e-8);
+      for (std::size_t t = 0; t <= std::min(its, r.iterations); ++t)
+        CHECK(rel(r.stress_trace[t], tr[t]) < 1e-10);
+      CHECK(r.step_seconds.size() == r.iterations);
+      for (std::size_t t = 1; t < r.stress_trace.size(); ++t)
+        CHECK(r.stress_trace[t] <= r.stress_trace[t - 1] + 1e-9);
+      // keep_config_trace walks the same iterates through the host loop
+      opt.keep_config_trace = true;
+      opt.max_iterations = 6;
+      const EmbeddingResult k = fjofc_embed(problem, spec, opt);
+      CHECK(k.config_trace.size() == k.iterations + 1);
+      CHECK(rel(k.stress_trace.back(), tr[k.iterations]) < 1e-10);
+    }
+  }
+}
+
+static void realizable_converges() {
+  // proj/tests/test_embed_core.cpp:277-292
+  Rng rng(45);
+  DenseMatrix x = random_matrix(rng, 10, 2);
+  center_columns(x);
+  const DenseMatrix delta = edm(x);
+  OmnibusProblem problem({delta, delta, delta});
+  SolveOptions opt;
+  opt.dim = 2;
+  opt.init = InitKind::provided;
+  opt.init_config = Configuration{{x, x, x}};
+  const EmbeddingResult r = fjofc_embed(problem, WeightSpec::uniform(1.0), opt);
+  CHECK(r.iterations <= 2);
+  CHECK(r.final_stress() < 1e-16);
+  CHECK(r.terminated == Termination::converged);
+}
+
+static void errors() {
+  Rng rng(48);
+  const OmnibusProblem problem = random_problem(rng, 5, 2, 2);
+  Configuration bad = random_config(rng, 5, 2, 2);
+  bad.blocks[0](0, 0) = std::numeric_limits<double>::quiet_NaN();
+  SolveOptions opt;
+  opt.dim = 2;
+  opt.init = InitKind::provided;
+  opt.init_config = bad;
+  CHECK(throws<NumericalError>([&] { fjofc_embed(problem, WeightSpec::uniform(1.0), opt); }));
+  const Configuration wrong = random_config(rng, 6, 2, 2);
+  CHECK(throws<std::invalid_argument>([&] { raw_stress(wrong, problem, WeightSpec::uniform(1.0)); }));
+  CHECK(throws<std::invalid_argument>(
+      [&] { guttman_step_fast(wrong, problem, WeightSpec::uniform(1.0)); }));
+  opt.init = InitKind::averaged_procrustes;
+  CHECK(throws<std::invalid_argument>([&] { fjofc_embed(problem, WeightSpec::uniform(1.0), opt); }));
+  DenseMatrix asym = problem.modality(0);
+  asym(0, 1) += 1.0;
+  CHECK(throws<std::invalid_argument>([&] { OmnibusProblem({asym}); }));
+  CHECK(throws<std::invalid_argument>([&] { WeightSpec::uniform(0.0); }));
+}
+
+static void out_of_sample() {
+  // proj/tests/test_oos.cpp:136-148 grid + embed + seed determinism
+  Rng rng(85);
+  for (std::size_t m : {1, 2, 4})
+    for (std::size_t n : {5, 9, 300})
+      for (std::size_t d : {1, 2, 3})
+        for (double w : {1.0, 10.0}) {
+          const Configuration x = random_config(rng, n, m, d);
+          OosDissimilarity deltas;
+          deltas.deltas.assign(m, std::vector<double>(n));
+          for (auto& v : deltas.deltas)
+            for (double& e : v) e = std::abs(rng.normal()) + 0.1;
+          const DenseMatrix y = random_matrix(rng, m, d, 1.5);
+          const auto xf = flat(x);
+          std::vector<double> df;
+          for (const auto& v : deltas.deltas) df.insert(df.end(), v.begin(), v.end());
+          std::vector<double> ref(m * d);
+          jo_oos_step_fast(m, n, d, y.data(), xf.data(), df.data(), w, ref.data());
+          const DenseMatrix got = oos_step_fast(y, x, deltas, w);
+          CHECK(rel_fro(std::vector<double>(got.data(), got.data() + got.size()), ref) < 1e-12);
+          double sref = 0.0;
+          jo_oos_stress(m, n, d, y.data(), xf.data(), df.data(), w, &sref);
+          CHECK(rel(oos_stress(y, x, deltas, w), sref) < 1e-12);
+          const OosResult e = oos_embed(x, deltas, w, OosOptions{1e-300, 60}, 11);
+          std::vector<double> ye(m * d), tr(61);
+          std::size_t its = 0;
+          int conv = 0;
+          jo_oos_embed(m, n, d, xf.data(), df.data(), w, 1e-300, 60, 11, ye.data(), tr.data(), &its,
+                       &conv);
+          CHECK(rel(e.stress_trace[0], tr[0]) < 1e-12);
+          if (e.iterations == its)
+            CHECK(rel_fro(std::vector<double>(e.y.data(), e.y.data() + e.y.size()), ye) < 1e-8);
+          const OosResult e2 = oos_embed(x, deltas, w, OosOptions{1e-300, 60}, 11);
+          CHECK(max_abs_diff(e.y, e2.y) == 0.0);
+        }
+}
+
+int main() {
+  fast_step_grid();
+  solve_trajectory();
+  realizable_converges();
+  errors();
+  out_of_sample();
+  std::printf("dropin_parity: %d checks, %d failures\n", g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}

@@ -1,0 +1,111 @@
+"""Packed layout and multi-GPU sharding, host side (CPU).
+
+* the stream enumerates every upper-triangle pair exactly once;
+* shard ranges partition the stream and balance block counts;
+* a world_size-2 gloo run: each rank forms the partial B(X)X products and
+  fidelity of ITS blocks only (numpy emulation of the pass kernel's
+  arithmetic contract), all-reduces them, applies the W^-1 mix, and must
+  reproduce the oracle's guttman_step_fast and raw_stress.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1502_03391_b200 import layout
+
+
+@pytest.mark.parametrize("n", [2, 3, 63, 64, 65, 127, 128, 129, 200, 1000])
+def test_stream_covers_upper_triangle_once(n):
+    seen = np.zeros((n, n), dtype=np.int32)
+    for _, B, J in layout.blocks(1, n):
+        r0, c0 = B * layout.ROWS, J * layout.COLS
+        for i in range(r0, min(r0 + layout.ROWS, n)):
+            j0 = max(c0, i + 1)
+            j1 = min(c0 + layout.COLS, n)
+            if j1 > j0:
+                seen[i, j0:j1] += 1
+    assert np.array_equal(seen, np.triu(np.ones((n, n), dtype=np.int32), 1))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shards_partition_and_balance(world):
+    m, n = 2, 20000
+    ranges = [layout.shard_range(m, n, r, world) for r in range(world)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == m * layout.geometry(n)[2]
+    for a, b in zip(ranges, ranges[1:]):
+        assert a[1] == b[0]
+    sizes = [hi - lo for lo, hi in ranges]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def partial_products(delta, x, within, m, n, rank, world):
+    """Row- and column-side B(X)X partials + weighted fidelity of one shard."""
+    P = np.zeros_like(x)
+    fid = 0.0
+    for l, B, J in layout.blocks(m, n, rank, world):
+        r0, c0 = B * layout.ROWS, J * layout.COLS
+        rows = np.arange(r0, min(r0 + layout.ROWS, n))
+        cols = np.arange(c0, min(c0 + layout.COLS, n))
+        if len(rows) == 0 or len(cols) == 0:
+            continue
+        I, Jj = np.meshgrid(rows, cols, indexing="ij")
+        mask = I < Jj
+        i, j = I[mask], Jj[mask]
+        diff = x[l, i] - x[l, j]
+        dist = np.sqrt(np.sum(diff * diff, axis=1))
+        dl = delta[l, i, j]
+        r = np.where(dist > 0, dl / np.where(dist > 0, dist, 1.0), 0.0)
+        contrib = r[:, None] * diff
+        np.add.at(P[l], i, contrib)
+        np.add.at(P[l], j, -contrib)
+        fid += within[l] * np.sum((dl - dist) ** 2)
+    return P, fid
+
+
+def _worker(rank, world, port, payload, out):
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    delta, x, within, coef, cross = payload
+    m, n, d = x.shape
+    P, fid = partial_products(delta, x, within, m, n, rank, world)
+    buf = torch.from_numpy(np.concatenate([P.ravel(), [fid]]))
+    dist.all_reduce(buf)
+    red = buf.numpy()
+    P, fid = red[:-1].reshape(m, n, d), red[-1]
+    xn = np.einsum("jl,lic->jic", coef, P)
+    com = sum(cross[a, b] * np.sum((x[a] - x[b]) ** 2)
+              for a in range(m) for b in range(a + 1, m))
+    out[rank] = (xn, fid + com)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_step_gloo_matches_oracle(world):
+    from oracle.oracle import Port, Spec
+    P = Port()
+    rng = np.random.default_rng(5)
+    m, n, d = 2, 300, 3
+    delta = np.stack([P.distance_matrix(rng.normal(size=(n, 3))) for _ in range(m)])
+    x = rng.normal(size=(m, n, d))
+    spec = Spec.uniform(0.5)
+    within, cross = P.weights_expand(spec, m)
+    winv = P.script_w_inverse(spec, m, n)
+    coef = winv * within[None, :]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = 29500 + os.getpid() % 1000
+    mp.spawn(_worker, args=(world, port, (delta, x, within, coef, cross), out), nprocs=world,
+             join=True)
+    ref_step = P.guttman_step_fast(delta, spec, x)
+    ref_stress = P.raw_stress(delta, spec, x)
+    for r in range(world):
+        xn, sigma = out[r]
+        assert np.linalg.norm(xn - ref_step) / np.linalg.norm(ref_step) < 1e-12
+        assert abs(sigma - ref_stress) / ref_stress < 1e-12
+    # both ranks hold identical results (the all-reduce is the only exchange)
+    assert np.array_equal(out[0][0], out[1][0])
