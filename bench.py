@@ -24,7 +24,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -163,16 +162,9 @@ def run_ours(args):
     dev.upload_features(wl.in_features)
     x0_host = wl.x0()
     x0_dev = torch.from_numpy(x0_host).cuda()
-    xbuf = None
     if world > 1:
-        count = lib.jofc_exchange_count(dev.h, wl.d)
-        xbuf = torch.zeros(count, dtype=torch.float64, device="cuda")
-        check(lib.jofc_set_exchange_buffer(dev.h, xbuf.data_ptr(), count))
-
-        def hook(ptr, cnt, strm):
-            with torch.cuda.stream(stream):
-                dist.all_reduce(xbuf[:cnt])
-        dev.set_allreduce(hook)
+        from paper_1502_03391_b200.dist import attach_nccl
+        attach_nccl(dev, wl.d)  # torch-owned exchange buffer, NCCL all-reduce on dev.stream
 
     import ctypes as C
     eps, T = 1e-300, wl.iterations
