@@ -113,39 +113,17 @@ double* exchange(jofc_ctx* c) {
 
 size_t fid_slot(const jofc_ctx* c) { return static_cast<size_t>(c->lay.m) * c->lay.n_pad * c->d; }
 
-template <int D, int VAR>
-int launch_pass_var(jofc_ctx* c, const PassParams& pp) {
+template <int D>
+int launch_pass(jofc_ctx* c, const PassParams& pp) {
   static bool attr_done = false;
   if (!attr_done) {
-    JOFC_CUDA(cudaFuncSetAttribute(jofc_pass_kernel<D, VAR>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+    JOFC_CUDA(cudaFuncSetAttribute(jofc_pass_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(sizeof(PassSmem<D>))));
     attr_done = true;
   }
-  jofc_pass_kernel<D, VAR><<<c->pass_grid, kPassThreads, sizeof(PassSmem<D>), c->stream>>>(pp);
+  jofc_pass_kernel<D><<<c->pass_grid, kPassThreads, sizeof(PassSmem<D>), c->stream>>>(pp);
   JOFC_CUDA(cudaGetLastError());
   return JOFC_OK;
-}
-
-int pass_variant() {
-  static int v = [] {
-    const char* e = getenv("JOFC_VARIANT");  // kernel-variant experiments
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-template <int D>
-int launch_pass(jofc_ctx* c, const PassParams& pp) {
-  if (D == 5 || D == 3) {
-    switch (pass_variant()) {
-      case 1: return launch_pass_var<D, 1>(c, pp);
-      case 2: return launch_pass_var<D, 2>(c, pp);
-      case 3: return launch_pass_var<D, 3>(c, pp);
-      default: break;
-    }
-  }
-  return launch_pass_var<D, 0>(c, pp);
 }
 
 template <int D>

@@ -267,7 +267,21 @@ __global__ void __launch_bounds__(256, 1) pair_math_kernel(double* out, int iter
           }
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          if (FL & 4) {
+          if (FL & 16) {
+            // seed without MUFU: s -> float by exponent rebias, magic-constant
+            // rsqrt + 2 FP32 Newton steps (~2^-17.7), float -> double rebias
+            const int hi = __double2hiint(s[g]), lo = __double2loint(s[g]);
+            const unsigned fb = (static_cast<unsigned>(hi - ((1023 - 127) << 20)) << 3) |
+                                (static_cast<unsigned>(lo) >> 29);
+            const float sf = __uint_as_float(fb);
+            float yf = __uint_as_float(0x5f3759dfu - (fb >> 1));
+            const float hs = 0.5f * sf;
+            yf = yf * fmaf(-hs * yf, yf, 1.5f);
+            yf = yf * fmaf(-hs * yf, yf, 1.5f);
+            const unsigned rb = __float_as_uint(yf);
+            y0[g] = __hiloint2double(static_cast<int>((rb >> 3) + ((1023 - 127) << 20)),
+                                     static_cast<int>(rb << 29));
+          } else if (FL & 4) {
             // fp32 seed: double -> float by exponent rebias (s in float range)
             const int hi = __double2hiint(s[g]), lo = __double2loint(s[g]);
             const unsigned fb = (static_cast<unsigned>(hi - ((1023 - 127) << 20)) << 3) |
@@ -356,7 +370,7 @@ extern "C" int jofc_probe_pair_math(int device, int d, int group, int flags,
   if (d == DD && group == GG && flags == FF) run_pair<DD, GG, FF>(sms, iters, buf, e0, e1, regs);
 #define JOFC_PM_ALL(FF) JOFC_PM(5, 4, FF) JOFC_PM(5, 1, FF) JOFC_PM(3, 4, FF) JOFC_PM(3, 1, FF)
   JOFC_PM_ALL(0) JOFC_PM_ALL(1) JOFC_PM_ALL(2) JOFC_PM_ALL(3) JOFC_PM_ALL(4) JOFC_PM_ALL(8)
-  JOFC_PM_ALL(12)
+  JOFC_PM_ALL(12) JOFC_PM_ALL(16)
 #undef JOFC_PM_ALL
 #undef JOFC_PM
   float ms = 0.f;
@@ -406,6 +420,17 @@ __global__ void __launch_bounds__(256) op_tput_kernel(double* out, int iters) {
         v[k] = fma(w1[0], w2[k], v[k]);
       } else if (OP == 7) {  // DADD, two fresh registers
         v[k] = v[k] + w2[k];
+      } else if (OP == 8) {  // 1 RSQ64H per 7 DFMA (pair-loop proportion), independent
+        if (k == 0) {
+          double r;
+          asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(w1[0]));
+          w1[0] = r + 1e-300;
+        } else {
+          v[k] = fma(v[k], 0.9999999, 1e-9);
+        }
+      } else if (OP == 9) {  // 8 DFMA + one 2-FSEL select per 8
+        v[k] = fma(v[k], 0.9999999, 1e-9);
+        if (k == 7) v[0] = (__double2hiint(v[7]) > 5) ? v[0] : 0.0;
       }
     }
   }
@@ -444,7 +469,9 @@ extern "C" int jofc_probe_op(int device, int op, double* per_clk_per_sm) {
     case 4: run(op_tput_kernel<4>); break;
     case 5: run(op_tput_kernel<5>); break;
     case 6: run(op_tput_kernel<6>); break;
-    default: run(op_tput_kernel<7>); break;
+    case 7: run(op_tput_kernel<7>); break;
+    case 8: run(op_tput_kernel<8>); break;
+    default: run(op_tput_kernel<9>); break;
   }
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);

@@ -19,16 +19,16 @@ for w in (4, 8, 12, 16, 32):
     print(f"warps/SM {w:2d}: chains 1,2,4,8,16 -> " + " ".join(row) + " TF/s")
 gp, regs = C.c_double(), C.c_int()
 names = {0: "full", 1: "no col acc", 2: "no fid", 3: "no col, no fid", 4: "fp32 seed",
-         8: "shared product", 12: "shared product + fp32 seed"}
+         8: "shared product", 12: "shared product + fp32 seed", 16: "magic + 2 fp32 Newton seed"}
 for d in (5, 3):
     for g in (1, 4):
-        for fl in (0, 1, 2, 3, 4, 8, 12):
+        for fl in (0, 16):
             lib.jofc_probe_pair_math(0, d, g, fl, C.byref(gp), C.byref(regs))
             print(f"pair math d={d} G={g} {names[fl]:28s}: {gp.value:7.1f} Gpairs/s ({regs.value} regs)"
                   f" C3-equiv pass {4e8 / (gp.value * 1e9) * 1e3:.3f} ms")
 pc = C.c_double()
 for op, name in ((0, "MUFU.RSQ64H"), (1, "MUFU.RSQ f32"), (2, "DADD"), (3, "DMUL"),
                  (4, "DFMA 3 regs"), (5, "DFMA 1 reg"), (6, "DFMA acc form"),
-                 (7, "DADD 2 regs")):
+                 (7, "DADD 2 regs"), (8, "7 DFMA + 1 RSQ64H"), (9, "8 DFMA + select")):
     lib.jofc_probe_op(0, op, C.byref(pc))
     print(f"{name:13s}: {pc.value:.3f} warp-instr/clk/SM (at max clock)")
