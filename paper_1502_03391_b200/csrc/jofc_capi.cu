@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "jofc_gpu.h"
@@ -99,6 +100,9 @@ struct jofc_ctx {
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
+  // CUDA graph of the whole launch sequence (single-GPU, no events)
+  std::map<std::vector<uintptr_t>, cudaGraphExec_t> graphs;
+  bool use_graphs = true;
   // oos state
   DevBuf<double> oos_x, oos_delta, oos_y0, oos_y1, oos_part, oos_trace;
   DevBuf<OosPoint> oos_st;
@@ -114,16 +118,28 @@ double* exchange(jofc_ctx* c) {
 size_t fid_slot(const jofc_ctx* c) { return static_cast<size_t>(c->lay.m) * c->lay.n_pad * c->d; }
 
 template <int D>
-int launch_pass(jofc_ctx* c, const PassParams& pp) {
+int setup_pass() {
   static bool attr_done = false;
   if (!attr_done) {
     JOFC_CUDA(cudaFuncSetAttribute(jofc_pass_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(sizeof(PassSmem<D>))));
     attr_done = true;
   }
+  return JOFC_OK;
+}
+
+template <int D>
+int launch_pass(jofc_ctx* c, const PassParams& pp) {
+  int rc = setup_pass<D>();
+  if (rc) return rc;
   jofc_pass_kernel<D><<<c->pass_grid, kPassThreads, sizeof(PassSmem<D>), c->stream>>>(pp);
   JOFC_CUDA(cudaGetLastError());
   return JOFC_OK;
+}
+
+template <int D>
+int setup_for(jofc_ctx*) {
+  return setup_pass<D>();
 }
 
 template <int D>
@@ -150,6 +166,7 @@ int launch_epi(jofc_ctx* c, const EpiParams& ep) {
   }
 
 int pass_for_d(jofc_ctx* c, const PassParams& pp) { JOFC_DISPATCH_D(c->d, launch_pass, c, pp); }
+int setup_for_d(jofc_ctx* c) { JOFC_DISPATCH_D(c->d, setup_for, c); }
 int epi_for_d(jofc_ctx* c, const EpiParams& ep) { JOFC_DISPATCH_D(c->d, launch_epi, c, ep); }
 
 int require_problem(jofc_ctx* c) {
@@ -290,6 +307,60 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   ep.n_pad = L.n_pad;
   ep.fid_slot = fid_slot(c);
 
+  // Single GPU, no per-launch events: replay a captured CUDA graph of the
+  // whole 2(max_it + 1)-kernel sequence (kernel parameters only hold buffer
+  // pointers; everything iteration-dependent lives in the control block).
+  const bool graphable = c->use_graphs && c->world == 1 && !events && !c->profiling;
+  if (graphable) {
+    std::vector<uintptr_t> key = {c->d, max_it, static_cast<uintptr_t>(c->pass_grid),
+                                  static_cast<uintptr_t>(c->epi_grid),
+                                  reinterpret_cast<uintptr_t>(pp.delta),
+                                  reinterpret_cast<uintptr_t>(pp.x0),
+                                  reinterpret_cast<uintptr_t>(pp.x1),
+                                  reinterpret_cast<uintptr_t>(pp.P),
+                                  reinterpret_cast<uintptr_t>(pp.ctrl),
+                                  reinterpret_cast<uintptr_t>(ep.trace),
+                                  reinterpret_cast<uintptr_t>(ep.com_partials),
+                                  reinterpret_cast<uintptr_t>(pp.fid_partials),
+                                  reinterpret_cast<uintptr_t>(ep.coef),
+                                  static_cast<uintptr_t>(L.n), static_cast<uintptr_t>(L.m),
+                                  static_cast<uintptr_t>(L.begin), static_cast<uintptr_t>(L.end),
+                                  static_cast<uintptr_t>(pp.diag)};
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+      if (c->graphs.size() >= 8) {
+        for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+        c->graphs.clear();
+      }
+      rc = setup_for_d(c);
+      if (rc) return rc;
+      JOFC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      int lrc = JOFC_OK;
+      for (size_t t = 0; t <= max_it && !lrc; ++t) {
+        lrc = pass_for_d(c, pp);
+        if (!lrc) lrc = epi_for_d(c, ep);
+      }
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+      if (lrc) {
+        if (g) cudaGraphDestroy(g);
+        return lrc;
+      }
+      if (ce != cudaSuccess)
+        return set_error(JOFC_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess)
+        return set_error(JOFC_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ie));
+      it = c->graphs.emplace(key, exec).first;
+    }
+    JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
+    c->launches += 2 * (max_it + 1);
+    c->max_it_enqueued = max_it;
+    return JOFC_OK;
+  }
+
   for (size_t t = 0; t <= max_it; ++t) {
     if (events) JOFC_CUDA(cudaEventRecord((*events)[t], c->stream));
     cudaEvent_t pe0 = nullptr, pe1 = nullptr;
@@ -384,6 +455,7 @@ int jofc_ctx_destroy(jofc_ctx* c) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   if (c->ctrl_host) cudaFreeHost(c->ctrl_host);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -751,13 +823,16 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
     JOFC_CUDA(cudaMemcpyAsync(stress0, c->oos_trace.p, sizeof(double), cudaMemcpyDeviceToHost,
                               c->stream));
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<double> y_all(y_out ? k * m * d : 0);
   for (size_t p = 0; p < k; ++p) {
     if (iterations) iterations[p] = static_cast<size_t>(st[p].iterations);
     if (y_out) {
       const double* src = (st[p].iterations & 1) ? yb.data() : ya.data();
-      std::memcpy(y_out + p * m * d, src + p * m * d, m * d * sizeof(double));
+      std::memcpy(y_all.data() + p * m * d, src + p * m * d, m * d * sizeof(double));
     }
   }
+  if (y_out)  // y_out may be host or device memory
+    JOFC_CUDA(cudaMemcpy(y_out, y_all.data(), y_all.size() * sizeof(double), cudaMemcpyDefault));
   return JOFC_OK;
 }
 
