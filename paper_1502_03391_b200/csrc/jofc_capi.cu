@@ -733,14 +733,51 @@ namespace {
 
 template <int D>
 int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
-  const dim3 pg((op.k + kOosWarps - 1) / kOosWarps, op.m);
+  const dim3 pg((op.k + kOosWarps - 1) / kOosWarps, op.m,
+                static_cast<unsigned>(std::min<long long>(kOosSplits, std::max<long long>(1, op.n / 256))));
   const unsigned ug = (op.k + 127) / 128;
-  for (int t = 0; t <= steps; ++t) {
-    jofc_oos_pass_kernel<D><<<pg, kOosWarps * 32, 0, c->stream>>>(op);
-    jofc_oos_update_kernel<D><<<ug, 128, 0, c->stream>>>(op);
-    c->launches += 2;
+  // The 2(steps + 1) launches are replayed from a captured CUDA graph (all
+  // per-step state is in the device-side point records).
+  std::vector<uintptr_t> key = {0x0005u, static_cast<uintptr_t>(D), static_cast<uintptr_t>(op.k),
+                                static_cast<uintptr_t>(op.m), static_cast<uintptr_t>(op.n),
+                                static_cast<uintptr_t>(steps), static_cast<uintptr_t>(op.fixed),
+                                static_cast<uintptr_t>(op.max_it),
+                                reinterpret_cast<uintptr_t>(op.x),
+                                reinterpret_cast<uintptr_t>(op.deltas),
+                                reinterpret_cast<uintptr_t>(op.y0),
+                                reinterpret_cast<uintptr_t>(op.y1),
+                                reinterpret_cast<uintptr_t>(op.part),
+                                reinterpret_cast<uintptr_t>(op.st),
+                                reinterpret_cast<uintptr_t>(op.traces)};
+  uint64_t wbits, ebits;
+  std::memcpy(&wbits, &op.w, 8);
+  std::memcpy(&ebits, &op.eps, 8);
+  key.push_back(static_cast<uintptr_t>(wbits));
+  key.push_back(static_cast<uintptr_t>(ebits));
+  auto it = c->graphs.find(key);
+  if (it == c->graphs.end()) {
+    if (c->graphs.size() >= 8) {
+      for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+      c->graphs.clear();
+    }
+    JOFC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (int t = 0; t <= steps; ++t) {
+      jofc_oos_pass_kernel<D><<<pg, kOosWarps * 32, 0, c->stream>>>(op);
+      jofc_oos_update_kernel<D><<<ug, 128, 0, c->stream>>>(op);
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    if (ce != cudaSuccess)
+      return set_error(JOFC_ECUDA, "oos graph capture failed: %s", cudaGetErrorString(ce));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess)
+      return set_error(JOFC_ECUDA, "oos graph instantiate failed: %s", cudaGetErrorString(ie));
+    it = c->graphs.emplace(key, exec).first;
   }
-  JOFC_CUDA(cudaGetLastError());
+  JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
+  c->launches += 2 * (steps + 1);
   return JOFC_OK;
 }
 
@@ -767,6 +804,7 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
   JOFC_CUDA(cudaMemcpyAsync(c->oos_y0.p, y0, k * m * d * sizeof(double), cudaMemcpyDefault,
                             c->stream));
   JOFC_CUDA(cudaMemsetAsync(c->oos_st.p, 0, k * sizeof(OosPoint), c->stream));
+  JOFC_CUDA(cudaMemsetAsync(c->oos_part.p, 0, (k * m * (d + 2) + k) * sizeof(double), c->stream));
   OosParams op{};
   op.x = c->oos_x.p;
   op.deltas = c->oos_delta.p;

@@ -11,7 +11,8 @@
 // closed-form corner update (proj/src/oos.cpp:98-111), the commensurability
 // term and the per-point stop rule (proj/src/oos.cpp:221-226).
 //
-// Pass layout: CTA = 8 warps = 8 points of one modality (blockIdx.y); X^(j)
+// Pass layout: CTA = 8 warps = 8 points of one modality (blockIdx.y) and one
+// of kOosSplits slices of the in-sample range (blockIdx.z); X^(j)
 // is staged through shared memory in 512-row chunks and shared by the 8
 // warps; lanes stride the n in-sample rows (coalesced delta reads), warp
 // shuffles finish the sums.
@@ -45,6 +46,7 @@ struct OosParams {
 
 constexpr int kOosWarps = 8;
 constexpr int kOosChunk = 512;
+constexpr int kOosSplits = 4;  // n-range slices per (point, modality): 4x the warps in flight
 
 template <int D>
 __global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_pass_kernel(const OosParams p) {
@@ -52,6 +54,8 @@ __global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_pass_kernel(const Oos
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pt = blockIdx.x * kOosWarps + warp;
   const int j = blockIdx.y;
+  const long long k_lo = p.n * blockIdx.z / gridDim.z;
+  const long long k_hi = p.n * (blockIdx.z + 1) / gridDim.z;
   bool active = pt < p.k;
   int t = 0;
   if (active) {
@@ -68,8 +72,8 @@ __global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_pass_kernel(const Oos
   double psi = 0.0, fid = 0.0, xi[D];
 #pragma unroll
   for (int c = 0; c < D; ++c) xi[c] = 0.0;
-  for (long long k0 = 0; k0 < p.n; k0 += kOosChunk) {
-    const int rows = static_cast<int>(min(static_cast<long long>(kOosChunk), p.n - k0));
+  for (long long k0 = k_lo; k0 < k_hi; k0 += kOosChunk) {
+    const int rows = static_cast<int>(min(static_cast<long long>(kOosChunk), k_hi - k0));
     __syncthreads();
     for (int e = threadIdx.x; e < rows * D; e += blockDim.x) xs[e] = X[k0 * D + e];
     __syncthreads();
@@ -101,12 +105,12 @@ __global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_pass_kernel(const Oos
 #pragma unroll
     for (int c = 0; c < D; ++c) xi[c] += __shfl_xor_sync(0xffffffffu, xi[c], o);
   }
-  if (lane == 0) {
+  if (lane == 0) {  // slices of the n range meet in `part` (zeroed by the update kernel)
     double* out = p.part + (static_cast<long long>(pt) * p.m + j) * (D + 2);
-    out[0] = psi;
-    out[1] = fid;
+    atomicAdd(out, psi);
+    atomicAdd(out + 1, fid);
 #pragma unroll
-    for (int c = 0; c < D; ++c) out[2 + c] = xi[c];
+    for (int c = 0; c < D; ++c) atomicAdd(out + 2 + c, xi[c]);
   }
 }
 
@@ -167,6 +171,8 @@ __global__ void __launch_bounds__(128) jofc_oos_update_kernel(const OosParams p)
                         spread * (xi_sum[c] + psi_y[c]);
     }
   }
+  double* pz = p.part + static_cast<long long>(pt) * m * (D + 2);
+  for (int e = 0; e < m * (D + 2); ++e) pz[e] = 0.0;
   st.t = t + 1;
   p.st[pt] = st;
 }

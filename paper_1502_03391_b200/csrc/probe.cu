@@ -481,3 +481,38 @@ extern "C" int jofc_probe_op(int device, int op, double* per_clk_per_sm) {
   cudaFree(buf);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
+
+// ------------------------------------------------- MUFU.RSQ64H seed accuracy
+namespace {
+__global__ void rsq_err_kernel(unsigned long long seed, int per_thread, double* out) {
+  unsigned long long x = seed ^ (0x9E3779B97F4A7C15ull * (blockIdx.x * blockDim.x + threadIdx.x + 1));
+  double worst = 0.0;
+  for (int i = 0; i < per_thread; ++i) {
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    const unsigned long long m = (x * 0x2545F4914F6CDD1Dull) >> 12;  // 52 random mantissa bits
+    const int ex = 1023 + static_cast<int>((x >> 5) % 80) - 40;      // s in ~[2^-40, 2^40)
+    const double s = __longlong_as_double((static_cast<long long>(ex) << 52) | m);
+    double y0;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(s));
+    const double e = fabs(fma(-(s * y0), y0, 1.0));
+    worst = fmax(worst, e);
+  }
+  for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned long long*>(out),
+                                         static_cast<unsigned long long>(__double_as_longlong(worst)));
+}
+}  // namespace
+
+// max |1 - s y0^2| of the MUFU.RSQ64H seed over random s (~2^26 samples)
+extern "C" int jofc_probe_rsq_error(int device, double* max_e) {
+  if (cudaSetDevice(device) != cudaSuccess) return 3;
+  double* d;
+  cudaMalloc(&d, sizeof(double));
+  cudaMemset(d, 0, sizeof(double));
+  rsq_err_kernel<<<1024, 256>>>(12345ull, 256, d);
+  cudaMemcpy(max_e, d, sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}

@@ -32,3 +32,9 @@ for op, name in ((0, "MUFU.RSQ64H"), (1, "MUFU.RSQ f32"), (2, "DADD"), (3, "DMUL
                  (7, "DADD 2 regs"), (8, "7 DFMA + 1 RSQ64H"), (9, "8 DFMA + select")):
     lib.jofc_probe_op(0, op, C.byref(pc))
     print(f"{name:13s}: {pc.value:.3f} warp-instr/clk/SM (at max clock)")
+me = C.c_double()
+lib.jofc_probe_rsq_error(0, C.byref(me))
+import math
+print(f"MUFU.RSQ64H seed: max |1 - s y0^2| = {me.value:.3e} (2^{math.log2(me.value):.2f}); "
+      f"2nd-order error ~ 3e^2/8 = {3 * me.value**2 / 8:.2e}, 3rd-order ~ 5e^3/16 = "
+      f"{5 * me.value**3 / 16:.2e}")
