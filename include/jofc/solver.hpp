@@ -11,8 +11,8 @@ namespace jofc {
 Configuration guttman_step_fast(const Configuration& config, const OmnibusProblem& problem,
                                 const WeightSpec& spec, bool parallel = false);
 
-// InitKind::provided only on this path; other inits throw std::invalid_argument
-// naming the missing initialiser.
+// InitKind::provided and InitKind::averaged_procrustes (the default; cMDS +
+// Procrustes on the GPU).  InitKind::imputed_cmds throws std::invalid_argument.
 EmbeddingResult fjofc_embed(const OmnibusProblem& problem, const WeightSpec& spec,
                             const SolveOptions& options);
 

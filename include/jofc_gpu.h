@@ -140,6 +140,14 @@ int jofc_oos_batch(jofc_ctx* ctx, size_t k, size_t m, size_t n, size_t d, const 
                    size_t max_it, int fixed_iterations, double* y_out, double* traces,
                    size_t* iterations);
 
+/* Initialisation on the resident problem (unsharded
+ * context): cmds of one modality, or of the modality average when
+ * modality < 0 (proj/src/init.cpp:21-42), x_out n x d; and
+ * averaged_procrustes_init (proj/src/init.cpp:57-88), x_out m x n x d -- the
+ * reference's default InitKind. */
+int jofc_cmds(jofc_ctx* ctx, int modality, size_t d, double* x_out);
+int jofc_init_averaged_procrustes(jofc_ctx* ctx, size_t d, double* x_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -365,6 +365,29 @@ class Reference:
         return EmbedResult(x, trace[: its.value + 1], its.value, bool(conv.value),
                            step_s.value, wall_s.value)
 
+    def cmds(self, delta, modality, d):
+        n = delta.shape[1]
+        out = np.empty((n, d))
+        self._check(self.lib.ref_cmds(self.problem(delta), int(modality), _sz(d), _ptr(out)))
+        return out
+
+    def averaged_procrustes_init(self, delta, d):
+        m, n, _ = delta.shape
+        out = np.empty((m, n, d))
+        self._check(self.lib.ref_averaged_procrustes_init(self.problem(delta), _sz(d), 1,
+                                                          _ptr(out)))
+        return out
+
+    def fjofc_embed_default_init(self, delta, spec, d, eps, max_it):
+        m, n, _ = delta.shape
+        x = np.empty((m, n, d))
+        trace = np.full(max_it + 1, np.nan)
+        its, conv = _sz(), C.c_int()
+        self._check(self.lib.ref_fjofc_embed_default_init(
+            self.problem(delta), C.byref(spec.c()), _sz(d), C.c_double(eps), _sz(max_it),
+            _ptr(x), _ptr(trace), C.byref(its), C.byref(conv)))
+        return EmbedResult(x, trace[: its.value + 1], its.value, bool(conv.value))
+
     def oos_stress(self, y, x, deltas, w):
         y, x, deltas = _f64(y), _f64(x), _f64(deltas)
         m, n, d = x.shape

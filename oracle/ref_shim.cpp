@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "jofc/distance.hpp"
+#include "jofc/init.hpp"
 #include "jofc/linalg.hpp"
 #include "jofc/oos.hpp"
 #include "jofc/problem.hpp"
@@ -225,6 +226,40 @@ int ref_fjofc_embed(void* prob, const jo_weights* spec, size_t d, const double* 
     double s = 0.0;
     for (double v : r.step_seconds) s += v;
     if (step_seconds_sum) *step_seconds_sum = s;
+  });
+}
+
+int ref_cmds(void* prob, int modality, size_t d, double* x_out) {
+  return guarded([&] {
+    const auto& p = *static_cast<OmnibusProblem*>(prob);
+    DenseMatrix x = cmds(p.modality(static_cast<size_t>(modality)), d);
+    std::memcpy(x_out, x.data(), x.size() * sizeof(double));
+  });
+}
+
+int ref_averaged_procrustes_init(void* prob, size_t d, int parallel, double* x_out) {
+  return guarded([&] {
+    const auto& p = *static_cast<OmnibusProblem*>(prob);
+    from_config(averaged_procrustes_init(p, d, parallel != 0), x_out);
+  });
+}
+
+// fjofc_embed with the default InitKind::averaged_procrustes
+int ref_fjofc_embed_default_init(void* prob, const jo_weights* spec, size_t d, double eps,
+                                 size_t max_it, double* x_out, double* trace_out,
+                                 size_t* iterations, int* converged) {
+  return guarded([&] {
+    const auto& p = *static_cast<OmnibusProblem*>(prob);
+    SolveOptions opt;
+    opt.dim = d;
+    opt.eps = eps;
+    opt.max_iterations = max_it;
+    opt.parallel = true;
+    EmbeddingResult r = fjofc_embed(p, make_spec(spec, p.modality_count()), opt);
+    from_config(r.config, x_out);
+    for (size_t i = 0; i < r.stress_trace.size(); ++i) trace_out[i] = r.stress_trace[i];
+    *iterations = r.iterations;
+    *converged = r.terminated == Termination::converged ? 1 : 0;
   });
 }
 

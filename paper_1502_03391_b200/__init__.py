@@ -14,6 +14,8 @@ from .api import (  # noqa: F401
     SolveOptions,
     Termination,
     WeightSpec,
+    averaged_procrustes_init,
+    cmds,
     default_device,
     fjofc_embed,
     guttman_step_fast,

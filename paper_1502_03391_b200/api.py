@@ -22,9 +22,9 @@ oos_embed                  oos_embed                 (oos.hpp:50-51)
 Configurations are numpy arrays of shape (m, n, d) (Configuration::blocks
 stacked).  Every call runs on the GPU through libjofc_gpu.so; the problem is
 packed into HBM once per OmnibusProblem and stays resident in the Device.
-InitKind::averaged_procrustes / imputed_cmds are outside this build's scope
-(SURVEY.md 8f row f1): they raise NotImplementedError instead of silently
-running something else.
+InitKind::averaged_procrustes (the reference default) runs on the GPU
+(cmds over the resident Delta); InitKind::imputed_cmds raises
+NotImplementedError.
 """
 from __future__ import annotations
 
@@ -331,23 +331,46 @@ def guttman_step_fast(config, problem, spec, parallel=False, device=None):
     return out
 
 
+def cmds(problem, modality, d, normalize=False, device=None):
+    """proj/src/init.cpp:21-42 on the GPU; modality < 0 = the modality average."""
+    dev = device or default_device()
+    dev.upload(problem, normalize=normalize)
+    out = np.empty((problem.object_count(), int(d)))
+    check(dev.lib.jofc_cmds(dev.h, int(modality), int(d), dptr(out)))
+    return out
+
+
+def averaged_procrustes_init(problem, d, normalize=False, device=None):
+    """proj/src/init.cpp:57-88 on the GPU (the reference's default init)."""
+    dev = device or default_device()
+    dev.upload(problem, normalize=normalize)
+    out = np.empty((problem.modality_count(), problem.object_count(), int(d)))
+    check(dev.lib.jofc_init_averaged_procrustes(dev.h, int(d), dptr(out)))
+    return out
+
+
 def fjofc_embed(problem, spec, options: SolveOptions, device=None):
-    """proj/src/solver.cpp:223-236 (+ run_majorization :106-150) on the GPU."""
-    if options.init != InitKind.provided:
-        raise NotImplementedError(
-            "only InitKind.provided is built on the GPU path (init is SURVEY.md 8f row f1)")
+    """proj/src/solver.cpp:223-236 (+ run_majorization :106-150) on the GPU.
+
+    InitKind.provided and InitKind.averaged_procrustes (the default, computed on
+    the GPU); InitKind.imputed_cmds is not built."""
     if options.dim < 1:
         raise InvalidArgument("SolveOptions: dim must be positive")
     if not options.eps > 0:
         raise InvalidArgument("SolveOptions: eps must be positive")
-    if options.init_config is None:
-        raise InvalidArgument("SolveOptions: provided init missing a configuration")
-    x0 = _f64(options.init_config)
     m, n = problem.modality_count(), problem.object_count()
-    if x0.shape != (m, n, options.dim):
-        raise InvalidArgument("SolveOptions: provided init has the wrong shape")
     dev = device or default_device()
-    dev.upload(problem, normalize=options.normalize)
+    if options.init == InitKind.provided:
+        if options.init_config is None:
+            raise InvalidArgument("SolveOptions: provided init missing a configuration")
+        x0 = _f64(options.init_config)
+        if x0.shape != (m, n, options.dim):
+            raise InvalidArgument("SolveOptions: provided init has the wrong shape")
+        dev.upload(problem, normalize=options.normalize)
+    elif options.init == InitKind.averaged_procrustes:
+        x0 = averaged_procrustes_init(problem, options.dim, options.normalize, device=dev)
+    else:
+        raise NotImplementedError("InitKind.imputed_cmds is not built on the GPU path")
     T = int(options.max_iterations)
     x = np.empty_like(x0)
     trace = np.empty(T + 1)

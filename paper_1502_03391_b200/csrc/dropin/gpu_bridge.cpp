@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "jofc/init.hpp"
 #include "jofc/linalg.hpp"
 #include "jofc/oos.hpp"
 #include "jofc/rng.hpp"
@@ -111,6 +112,22 @@ Configuration unflatten(const std::vector<double>& x, std::size_t m, std::size_t
 
 void set_device(int device) { t_device = device; }
 
+Configuration averaged_procrustes_init(const OmnibusProblem& problem, std::size_t d, bool) {
+  Ctx& c = with_problem(problem, false);
+  std::vector<double> x(problem.modality_count() * problem.object_count() * d);
+  check(jofc_init_averaged_procrustes(c.h, d, x.data()));
+  return unflatten(x, problem.modality_count(), problem.object_count(), d);
+}
+
+DenseMatrix cmds(const DenseMatrix& delta, std::size_t d) {
+  // one-modality problem, its own (short-lived) residency
+  OmnibusProblem single({delta});
+  Ctx& c = with_problem(single, false);
+  DenseMatrix out(delta.rows(), d);
+  check(jofc_cmds(c.h, 0, d, out.data()));
+  return out;
+}
+
 double stress_pair_count(std::size_t m, std::size_t n) {
   const double mn = static_cast<double>(m) * static_cast<double>(n);
   return mn * (mn - 1.0) / 2.0;
@@ -156,14 +173,24 @@ EmbeddingResult fjofc_embed(const OmnibusProblem& problem, const WeightSpec& spe
   spec.validate(problem.modality_count());
   if (options.dim < 1) throw std::invalid_argument("SolveOptions: dim must be positive");
   if (!(options.eps > 0.0)) throw std::invalid_argument("SolveOptions: eps must be positive");
-  if (options.init != InitKind::provided)
-    throw std::invalid_argument(
-        "fjofc_embed: only InitKind::provided runs on the GPU path (averaged_procrustes / "
-        "imputed_cmds initialisers are not part of this build)");
-  if (!options.init_config)
-    throw std::invalid_argument("SolveOptions: provided init missing a configuration");
-  const Configuration& x0 = *options.init_config;
   const std::size_t m = problem.modality_count(), n = problem.object_count(), d = options.dim;
+  Configuration start;
+  if (options.init == InitKind::averaged_procrustes) {
+    // the reference default, computed on the GPU from the resident Delta
+    Ctx& c = with_problem(problem, options.normalize);
+    std::vector<double> x(m * n * d);
+    check(jofc_init_averaged_procrustes(c.h, d, x.data()));
+    start = unflatten(x, m, n, d);
+  } else if (options.init == InitKind::imputed_cmds) {
+    throw std::invalid_argument(
+        "fjofc_embed: InitKind::imputed_cmds is not part of this build (use "
+        "averaged_procrustes or provided)");
+  } else {
+    if (!options.init_config)
+      throw std::invalid_argument("SolveOptions: provided init missing a configuration");
+    start = *options.init_config;
+  }
+  const Configuration& x0 = start;
   if (x0.modality_count() != m || x0.object_count() != n || x0.dim() != d)
     throw std::invalid_argument("SolveOptions: provided init has the wrong shape");
   for (const DenseMatrix& b : x0.blocks)

@@ -24,6 +24,7 @@
 #include "jofc_gpu.h"
 #include "jofc_kernels.cuh"
 #include "jofc_oos.cuh"
+#include "jofc_init.cuh"
 #include "jofc_weights.h"
 
 using namespace jofc_gpu;
@@ -893,6 +894,238 @@ int jofc_oos_stress(jofc_ctx* c, size_t m, size_t n, size_t d, const double* y, 
 int jofc_oos_step(jofc_ctx* c, size_t m, size_t n, size_t d, const double* y, const double* x,
                   const double* deltas, double w, double* y_next) {
   return oos_run(c, 1, m, n, d, x, deltas, w, y, 1.0, 1, 1, y_next, nullptr, nullptr, nullptr);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- initialisation
+namespace {
+
+template <int P>
+void launch_matvec(const double* S, long long n, const double* q, double* z, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>((n * 32 + 255) / 256);
+  init::matvec_kernel<P><<<grid, 256, 0, st>>>(S, n, q, z);
+}
+
+int matvec_p(int p, const double* S, long long n, const double* q, double* z, cudaStream_t st) {
+  switch (p) {
+    case 5: launch_matvec<5>(S, n, q, z, st); break;
+    case 6: launch_matvec<6>(S, n, q, z, st); break;
+    case 7: launch_matvec<7>(S, n, q, z, st); break;
+    case 8: launch_matvec<8>(S, n, q, z, st); break;
+    case 9: launch_matvec<9>(S, n, q, z, st); break;
+    case 10: launch_matvec<10>(S, n, q, z, st); break;
+    case 11: launch_matvec<11>(S, n, q, z, st); break;
+    case 12: launch_matvec<12>(S, n, q, z, st); break;
+    case 13: launch_matvec<13>(S, n, q, z, st); break;
+    case 14: launch_matvec<14>(S, n, q, z, st); break;
+    default: return set_error(JOFC_EINVAL, "cmds: subspace width %d unsupported", p);
+  }
+  JOFC_CUDA(cudaGetLastError());
+  return JOFC_OK;
+}
+
+// cmds (proj/src/init.cpp:21-42) of modality `which` (< 0: the modality
+// average) of the resident problem; x is n x d row-major.
+int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
+  const Layout& L = c->lay;
+  const long long n = L.n;
+  if (d < 1 || static_cast<long long>(d) > n)
+    return set_error(JOFC_EINVAL, "cmds: dimension out of range");
+  DevBuf<double> S, aux;
+  JOFC_CUDA(S.ensure(static_cast<size_t>(n) * n));
+  JOFC_CUDA(aux.ensure(static_cast<size_t>(n) + 1));
+  JOFC_CUDA(cudaMemsetAsync(S.p, 0, static_cast<size_t>(n) * n * sizeof(double), c->stream));
+  init::dense_d2_kernel<<<static_cast<unsigned>(L.bpm), 256, 0, c->stream>>>(
+      c->delta.p, n, L.nT, L.bpm, L.m, which, S.p);
+  JOFC_CUDA(cudaGetLastError());
+  init::row_sums_kernel<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, c->stream>>>(S.p, n,
+                                                                                          aux.p);
+  JOFC_CUDA(cudaGetLastError());
+  std::vector<double> rs(n);
+  JOFC_CUDA(cudaMemcpyAsync(rs.data(), aux.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  const double inv_n = 1.0 / static_cast<double>(n);
+  double total = 0.0;
+  for (long long i = 0; i < n; ++i) {
+    total += rs[i];
+    rs[i] *= inv_n;
+  }
+  total *= inv_n * inv_n;
+  JOFC_CUDA(cudaMemcpyAsync(aux.p, rs.data(), n * sizeof(double), cudaMemcpyHostToDevice,
+                            c->stream));
+  DevBuf<double> fro2;
+  JOFC_CUDA(fro2.ensure(1));
+  JOFC_CUDA(cudaMemsetAsync(fro2.p, 0, sizeof(double), c->stream));
+  init::double_center_kernel<<<static_cast<unsigned>(c->num_sms * 8), 256, 0, c->stream>>>(
+      S.p, n, aux.p, total, fro2.p);
+  JOFC_CUDA(cudaGetLastError());
+  c->launches += 3;
+  double f2 = 0.0;
+  JOFC_CUDA(cudaMemcpyAsync(&f2, fro2.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  const double snorm = std::sqrt(f2);
+
+  const size_t k = d;
+  std::vector<double> values(k);
+  init::Mat vecs(n, k);
+  if (n <= 320 || k + 4 >= static_cast<size_t>(n)) {
+    // the reference's dense route (cyclic Jacobi on the whole S)
+    init::Mat h(n, n);
+    JOFC_CUDA(cudaMemcpy(h.a.data(), S.p, h.a.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<double> ev;
+    init::Mat v;
+    if (!init::jacobi_eigen(h, ev, v))
+      return set_error(JOFC_ENUMERIC, "jacobi eigensolver did not converge within the sweep cap");
+    std::vector<size_t> order(n);
+    std::iota(order.begin(), order.end(), size_t{0});
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return ev[a] > ev[b]; });
+    for (size_t cc = 0; cc < k; ++cc) {
+      std::vector<double> col(n);
+      for (long long r = 0; r < n; ++r) col[r] = v(r, order[cc]);
+      init::fix_sign(col);
+      values[cc] = ev[order[cc]];
+      for (long long r = 0; r < n; ++r) vecs(r, cc) = col[r];
+    }
+  } else if (snorm == 0.0) {
+    for (size_t cc = 0; cc < k; ++cc) {
+      values[cc] = 0.0;
+      vecs(cc, cc) = 1.0;
+    }
+  } else {
+    // shifted orthogonal iteration with Rayleigh-Ritz (proj/src/linalg.cpp:167-271)
+    const size_t p = k + 4;
+    const double shift = snorm, tol = 1e-9 * snorm;
+    init::Mat q(n, p), z(n, p);
+    init::Normals rng(0x9e3779b97f4a7c15ull);
+    for (double& v : q.a) v = rng.next();
+    init::orthonormalize(q);
+    DevBuf<double> dq, dz;
+    JOFC_CUDA(dq.ensure(q.a.size()));
+    JOFC_CUDA(dz.ensure(q.a.size()));
+    bool done = false;
+    for (int iter = 0; iter < 5000 && !done; ++iter) {
+      JOFC_CUDA(cudaMemcpyAsync(dq.p, q.a.data(), q.a.size() * sizeof(double),
+                                cudaMemcpyHostToDevice, c->stream));
+      int rc = matvec_p(static_cast<int>(p), S.p, n, dq.p, dz.p, c->stream);
+      if (rc) return rc;
+      ++c->launches;
+      JOFC_CUDA(cudaMemcpyAsync(z.a.data(), dz.p, z.a.size() * sizeof(double),
+                                cudaMemcpyDeviceToHost, c->stream));
+      JOFC_CUDA(cudaStreamSynchronize(c->stream));
+      init::Mat t(p, p);
+      for (size_t i = 0; i < p; ++i)
+        for (size_t j = 0; j < p; ++j) {
+          double dot = 0.0;
+          for (long long r = 0; r < n; ++r) dot += q(r, i) * z(r, j);
+          t(i, j) = dot;
+        }
+      for (size_t i = 0; i < p; ++i)
+        for (size_t j = i + 1; j < p; ++j) t(i, j) = t(j, i) = 0.5 * (t(i, j) + t(j, i));
+      std::vector<double> theta;
+      init::Mat u;
+      if (!init::jacobi_eigen(t, theta, u))
+        return set_error(JOFC_ENUMERIC, "jacobi eigensolver did not converge within the sweep cap");
+      std::vector<size_t> order(p);
+      std::iota(order.begin(), order.end(), size_t{0});
+      std::stable_sort(order.begin(), order.end(),
+                       [&](size_t a, size_t b) { return theta[a] > theta[b]; });
+      bool conv = true;
+      init::Mat ritz(n, k);
+      for (size_t cc = 0; cc < k && conv; ++cc) {
+        const size_t col = order[cc];
+        double res2 = 0.0;
+        for (long long r = 0; r < n; ++r) {
+          double rv = 0.0, zv = 0.0;
+          for (size_t j = 0; j < p; ++j) {
+            rv += q(r, j) * u(j, col);
+            zv += z(r, j) * u(j, col);
+          }
+          ritz(r, cc) = rv;
+          const double df = zv - theta[col] * rv;
+          res2 += df * df;
+        }
+        values[cc] = theta[col];
+        if (std::sqrt(res2) > tol) conv = false;
+      }
+      if (conv) {
+        for (size_t cc = 0; cc < k; ++cc) {
+          std::vector<double> col(n);
+          double nr = 0.0;
+          for (long long r = 0; r < n; ++r) {
+            col[r] = ritz(r, cc);
+            nr += col[r] * col[r];
+          }
+          nr = std::sqrt(nr);
+          for (double& v : col) v /= nr;
+          init::fix_sign(col);
+          for (long long r = 0; r < n; ++r) vecs(r, cc) = col[r];
+        }
+        done = true;
+        break;
+      }
+      for (size_t i = 0; i < z.a.size(); ++i) z.a[i] += shift * q.a[i];
+      q = z;
+      init::orthonormalize(q);
+    }
+    if (!done)
+      return set_error(JOFC_ENUMERIC,
+                       "subspace eigensolver did not converge within the iteration cap");
+  }
+  x = init::Mat(n, d);
+  for (size_t cc = 0; cc < d; ++cc) {
+    const double sc = std::sqrt(std::max(values[cc], 0.0));  // Torgerson clamp
+    for (long long r = 0; r < n; ++r) x(r, cc) = sc * vecs(r, cc);
+  }
+  init::center_columns(x);
+  return JOFC_OK;
+}
+
+int require_full_problem(jofc_ctx* c) {
+  int rc = require_problem(c);
+  if (rc) return rc;
+  if (c->world != 1)
+    return set_error(JOFC_EINVAL, "initialisation needs an unsharded context (whole Delta)");
+  return JOFC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int jofc_cmds(jofc_ctx* c, int modality, size_t d, double* x_out) {
+  int rc = require_full_problem(c);
+  if (rc) return rc;
+  if (modality >= c->lay.m) return set_error(JOFC_EINVAL, "cmds: modality out of range");
+  JOFC_CUDA(cudaSetDevice(c->device));
+  init::Mat x;
+  rc = cmds_gpu(c, modality, d, x);
+  if (rc) return rc;
+  JOFC_CUDA(cudaMemcpy(x_out, x.a.data(), x.a.size() * sizeof(double), cudaMemcpyDefault));
+  return JOFC_OK;
+}
+
+int jofc_init_averaged_procrustes(jofc_ctx* c, size_t d, double* x_out) {
+  int rc = require_full_problem(c);
+  if (rc) return rc;
+  JOFC_CUDA(cudaSetDevice(c->device));
+  init::Mat anchor;
+  rc = cmds_gpu(c, -1, d, anchor);
+  if (rc) return rc;
+  init::center_columns(anchor);
+  const size_t block = static_cast<size_t>(c->lay.n) * d;
+  std::vector<double> out(static_cast<size_t>(c->lay.m) * block);
+  for (int l = 0; l < c->lay.m; ++l) {
+    init::Mat xl;
+    rc = cmds_gpu(c, l, d, xl);
+    if (rc) return rc;
+    init::center_columns(xl);
+    const init::Mat rot = init::procrustes(xl, anchor);
+    std::copy(rot.a.begin(), rot.a.end(), out.begin() + l * block);
+  }
+  JOFC_CUDA(cudaMemcpy(x_out, out.data(), out.size() * sizeof(double), cudaMemcpyDefault));
+  return JOFC_OK;
 }
 
 }  // extern "C"

@@ -428,6 +428,17 @@ __global__ void __launch_bounds__(256) op_tput_kernel(double* out, int iters) {
         } else {
           v[k] = fma(v[k], 0.9999999, 1e-9);
         }
+      } else if (OP == 10) {  // F2F.F32.F64
+        f[k] = __double2float_rn(v[k]) + f[k];
+        v[k] = v[k] * 1.0000001;
+      } else if (OP == 11) {  // 7 DFMA + 1 (F2F.F32.F64, MUFU.RSQ f32, F2F.F64.F32)
+        if (k == 0) {
+          float t;
+          asm volatile("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(__double2float_rn(w1[0])));
+          w1[0] = static_cast<double>(t) + 1e-300;
+        } else {
+          v[k] = fma(v[k], 0.9999999, 1e-9);
+        }
       } else if (OP == 9) {  // 8 DFMA + one 2-FSEL select per 8
         v[k] = fma(v[k], 0.9999999, 1e-9);
         if (k == 7) v[0] = (__double2hiint(v[7]) > 5) ? v[0] : 0.0;
@@ -471,7 +482,9 @@ extern "C" int jofc_probe_op(int device, int op, double* per_clk_per_sm) {
     case 6: run(op_tput_kernel<6>); break;
     case 7: run(op_tput_kernel<7>); break;
     case 8: run(op_tput_kernel<8>); break;
-    default: run(op_tput_kernel<9>); break;
+    case 9: run(op_tput_kernel<9>); break;
+    case 10: run(op_tput_kernel<10>); break;
+    default: run(op_tput_kernel<11>); break;
   }
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);

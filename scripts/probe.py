@@ -29,7 +29,8 @@ for d in (5, 3):
 pc = C.c_double()
 for op, name in ((0, "MUFU.RSQ64H"), (1, "MUFU.RSQ f32"), (2, "DADD"), (3, "DMUL"),
                  (4, "DFMA 3 regs"), (5, "DFMA 1 reg"), (6, "DFMA acc form"),
-                 (7, "DADD 2 regs"), (8, "7 DFMA + 1 RSQ64H"), (9, "8 DFMA + select")):
+                 (7, "DADD 2 regs"), (8, "7 DFMA + 1 RSQ64H"), (9, "8 DFMA + select"),
+                 (10, "F2F.F32.F64+DMUL"), (11, "7 DFMA + F2F,RSQf32,F2F")):
     lib.jofc_probe_op(0, op, C.byref(pc))
     print(f"{name:13s}: {pc.value:.3f} warp-instr/clk/SM (at max clock)")
 me = C.c_double()

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "jofc/init.hpp"
 #include "jofc/linalg.hpp"
 #include "jofc/oos.hpp"
 #include "jofc/rng.hpp"
@@ -189,6 +190,24 @@ static void solve_trajectory() {
   }
 }
 
+static void default_init_runs() {
+  // fjofc_embed with default SolveOptions (InitKind::averaged_procrustes) now
+  // works end to end; the trace decreases from the cMDS start.
+  Rng rng(77);
+  const OmnibusProblem problem = random_problem(rng, 120, 2, 3);
+  SolveOptions opt;
+  opt.dim = 2;
+  opt.max_iterations = 50;
+  const EmbeddingResult r = fjofc_embed(problem, WeightSpec::uniform(1.0), opt);
+  CHECK(r.iterations >= 1);
+  for (std::size_t t = 1; t < r.stress_trace.size(); ++t)
+    CHECK(r.stress_trace[t] <= r.stress_trace[t - 1] + 1e-9);
+  const Configuration init = averaged_procrustes_init(problem, 2);
+  CHECK(init.modality_count() == 2 && init.object_count() == 120 && init.dim() == 2);
+  CHECK(std::abs(raw_stress(init, problem, WeightSpec::uniform(1.0)) - r.stress_trace[0]) <=
+        1e-10 * r.stress_trace[0]);
+}
+
 static void realizable_converges() {
   // proj/tests/test_embed_core.cpp:277-292
   Rng rng(45);
@@ -220,7 +239,7 @@ static void errors() {
   CHECK(throws<std::invalid_argument>([&] { raw_stress(wrong, problem, WeightSpec::uniform(1.0)); }));
   CHECK(throws<std::invalid_argument>(
       [&] { guttman_step_fast(wrong, problem, WeightSpec::uniform(1.0)); }));
-  opt.init = InitKind::averaged_procrustes;
+  opt.init = InitKind::imputed_cmds;
   CHECK(throws<std::invalid_argument>([&] { fjofc_embed(problem, WeightSpec::uniform(1.0), opt); }));
   DenseMatrix asym = problem.modality(0);
   asym(0, 1) += 1.0;
@@ -269,6 +288,7 @@ int main() {
   fast_step_grid();
   solve_trajectory();
   realizable_converges();
+  default_init_runs();
   errors();
   out_of_sample();
   std::printf("dropin_parity: %d checks, %d failures\n", g_checks, g_fail);

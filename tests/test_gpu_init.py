@@ -1,0 +1,57 @@
+"""GPU initialisation against the real reference:
+cmds (proj/src/init.cpp:21-42), averaged_procrustes_init (:57-88) and
+fjofc_embed with the default InitKind."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1502_03391_b200 as jg
+from conftest import rel_fro
+from oracle.oracle import REF_SO, Port, Spec
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not os.path.exists(REF_SO), reason="oracle/_ref not built")]
+
+
+@pytest.fixture(scope="module")
+def R():
+    from oracle.oracle import Reference
+    return Reference()
+
+
+def problem(n, m=2, seed=3, p=4):
+    P = Port()
+    rng = np.random.default_rng(seed)
+    z = rng.normal(size=(n, p))
+    return np.stack([P.distance_matrix(z + 0.1 * rng.normal(size=(n, p))) for _ in range(m)])
+
+
+@pytest.mark.parametrize("n,tol", [(40, 1e-12), (300, 1e-12), (500, 1e-7), (1200, 1e-7)])
+def test_cmds_matches_reference(R, n, tol):
+    delta = problem(n)
+    prob = jg.OmnibusProblem(list(delta), validate=False)
+    for d in (1, 2, 3):
+        ref = R.cmds(delta, 0, d)
+        got = jg.cmds(prob, 0, d)
+        assert rel_fro(got, ref) < tol, (n, d, rel_fro(got, ref))
+
+
+@pytest.mark.parametrize("n,tol", [(60, 1e-12), (400, 1e-7)])
+def test_averaged_procrustes_init_matches_reference(R, n, tol):
+    delta = problem(n, m=3, seed=9)
+    prob = jg.OmnibusProblem(list(delta), validate=False)
+    ref = R.averaged_procrustes_init(delta, 2)
+    got = jg.averaged_procrustes_init(prob, 2)
+    assert rel_fro(got, ref) < tol, rel_fro(got, ref)
+
+
+def test_default_init_solve_matches_reference(R):
+    delta = problem(250, m=2, seed=11)
+    prob = jg.OmnibusProblem(list(delta), validate=False)
+    opt = jg.SolveOptions(dim=2, eps=1e-300, max_iterations=40)  # default InitKind
+    got = jg.fjofc_embed(prob, jg.WeightSpec.uniform(0.5), opt)
+    ref = R.fjofc_embed_default_init(delta, Spec.uniform(0.5), 2, 1e-300, 40)
+    assert got.iterations == ref.iterations
+    assert rel_fro(got.config, ref.x) < 1e-8
+    assert max(abs(a - b) / abs(b) for a, b in zip(got.stress_trace, ref.trace)) < 1e-10
