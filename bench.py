@@ -549,6 +549,123 @@ def run_oos(args):
     dev.close()
 
 
+def run_init(args):
+    """the reference's default initialiser
+    (averaged_procrustes_init, proj/src/init.cpp:57-88) on the resident Delta.
+    One step = one whole init (m + 1 cMDS subspace iterations + Procrustes)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_1502_03391_b200 as jg
+    from paper_1502_03391_b200 import workloads
+    from paper_1502_03391_b200._capi import check, dptr
+
+    rank, world, local = env_rank()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    wl = workloads.make(args.config)
+    m, n, d = wl.m, wl.n, wl.d
+    dev = jg.Device(local)
+    lib = dev.lib
+    dev.upload_features(wl.in_features)
+    out = np.empty((m, n, d))
+
+    def step():
+        check(lib.jofc_init_averaged_procrustes(dev.h, d, dptr(out)))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = dev.launches()
+    check(lib.jofc_profile(dev.h, 1))
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    clk = clocks.stop()
+    launches = dev.launches() - launches0
+    mv_ms, mv_n = C.c_double(), C.c_uint64()
+    check(lib.jofc_profile_read(dev.h, C.byref(mv_ms), C.byref(mv_n)))
+    check(lib.jofc_profile(dev.h, 0))
+    sweeps = mv_n.value / args.steps
+    mv_share = mv_ms.value / (sec * 1e3)
+    mv_avg_ms = mv_ms.value / max(1, mv_n.value)
+    s_bytes = n * n * 8  # the dense double-centred S streamed once per sweep
+    achieved = s_bytes / (mv_avg_ms * 1e-3) / 1e9
+    hbm_peak, hbm_src = measured_peaks()
+    # e2e: host Delta through the public API (dense H2D + pack, init, D2H of X)
+    e2e = None
+    delta = wl.dense_delta() if not (args.no_e2e and args.no_cpu_baseline) else None
+    if not args.no_e2e:
+        mods = list(delta)
+        e2e_steps = max(1, args.e2e_steps)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            prob = jg.OmnibusProblem(mods, validate=False)
+            jg.averaged_procrustes_init(prob, d, device=dev)
+        e2e_sec = (time.perf_counter() - t0) / e2e_steps
+        e2e = {"value": round(1.0 / e2e_sec, 4), "unit": "inits/s",
+               "h2d_bytes_per_step": int(sum(x.nbytes for x in mods)),
+               "d2h_bytes_per_step": int(out.nbytes)}
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle.oracle import Port, Reference
+        try:
+            R = Reference()
+        except (FileNotFoundError, OSError):
+            R = None
+        if R is not None:
+            R.problem(delta)
+            # bounded sample: the cMDS of the modality average, one of the m + 1
+            # eigen-solves of the init, timed whole; its sweep count is the GPU's
+            # (same iteration, same start)
+            check(lib.jofc_profile(dev.h, 1))
+            xa = np.empty((n, d))
+            check(lib.jofc_cmds(dev.h, -1, d, dptr(xa)))
+            check(lib.jofc_profile_read(dev.h, C.byref(mv_ms), C.byref(mv_n)))
+            check(lib.jofc_profile(dev.h, 0))
+            t0 = time.perf_counter()
+            R.cmds(delta, -1, d)
+            csec = time.perf_counter() - t0
+            cpu = {"value": round(mv_n.value / csec, 3), "unit": "sweeps/s", "kind": "reference",
+                   "cores": R.max_threads(),
+                   "sample": f"jofc_ref::cmds of the modality average ({mv_n.value} subspace "
+                             f"sweeps at n={n}, p={d + 4}; OpenMP), call wall time",
+                   "seconds": round(csec, 3)}
+            R.release()
+    line = {
+        "metric": f"averaged_procrustes_init (fJOFC default init) per second, "
+                  f"{CONFIG_NAMES[wl.cfg]}",
+        "value": round(args.steps / sec, 4), "unit": "inits/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(sec / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "replicas only", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md)",
+        "config": {"workload": f"{CONFIG_NAMES[wl.cfg]} init: m+1={m + 1} cMDS eigen-solves "
+                               f"(shifted subspace iteration, p={d + 4}) + Procrustes",
+                   "l2": f"S is {s_bytes / 1e9:.2f} GB per solve, larger than L2"},
+        "sweeps_per_s": round(sweeps * args.steps / sec, 1), "sweeps_per_init": sweeps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "peak_source": hbm_src, "kernel": "matvec_sym_kernel (S Q)",
+                     "kernel_ms": round(mv_avg_ms, 4),
+                     "share_of_step": round(mv_share, 4)},
+        "gpu_launches": int(launches), "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if cpu:
+        line["cpu_baseline"] = cpu
+        line["sweeps_per_s_vs_cpu"] = round(line["sweeps_per_s"] / cpu["value"], 1)
+    print(json.dumps(line), flush=True)
+    dev.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -562,6 +679,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-iterations", type=int, default=2)
     ap.add_argument("--oos", action="store_true", help="C5 out-of-sample batch (config 5)")
+    ap.add_argument("--init", action="store_true",
+                    help="averaged_procrustes_init on the resident Delta (SURVEY 8f row f1)")
     ap.add_argument("--graphs", type=int, default=None,
                     help="replay CUDA graphs in the timed region (default: on for configs 1,2,5)")
     args = ap.parse_args()
@@ -573,6 +692,8 @@ def main():
         run_reference(args)
     elif args.oos:
         run_oos(args)
+    elif args.init:
+        run_init(args)
     else:
         run_ours(args)
 

@@ -232,7 +232,20 @@ int ref_fjofc_embed(void* prob, const jo_weights* spec, size_t d, const double* 
 int ref_cmds(void* prob, int modality, size_t d, double* x_out) {
   return guarded([&] {
     const auto& p = *static_cast<OmnibusProblem*>(prob);
-    DenseMatrix x = cmds(p.modality(static_cast<size_t>(modality)), d);
+    if (modality >= static_cast<int>(p.modality_count()))
+      throw std::invalid_argument("cmds: modality out of range");
+    DenseMatrix x;
+    if (modality < 0) {  // the average, built as averaged_procrustes_init does
+      const size_t n = p.object_count();
+      DenseMatrix average(n, n);
+      for (size_t l = 0; l < p.modality_count(); ++l)
+        for (size_t i = 0; i < average.size(); ++i) average.data()[i] += p.modality(l).data()[i];
+      for (size_t i = 0; i < average.size(); ++i)
+        average.data()[i] /= static_cast<double>(p.modality_count());
+      x = cmds(average, d);
+    } else {
+      x = cmds(p.modality(static_cast<size_t>(modality)), d);
+    }
     std::memcpy(x_out, x.data(), x.size() * sizeof(double));
   });
 }

@@ -11,6 +11,8 @@
 // and later launches exit at entry once the control block says done.
 #include <cuda_runtime.h>
 
+#include <chrono>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -57,6 +59,10 @@ template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
   cudaError_t ensure(size_t count) {
     if (count <= n && p) return cudaSuccess;
     if (p) cudaFree(p);
@@ -165,6 +171,23 @@ int launch_epi(jofc_ctx* c, const EpiParams& ep) {
     default:                                \
       return set_error(JOFC_EINVAL, "dim %zu unsupported (1..10)", static_cast<size_t>(d)); \
   }
+
+// When profiling, records the start event of the next profiled launch on the
+// context stream and hands back its end event (else leaves *end null).
+int prof_begin(jofc_ctx* c, cudaEvent_t* end) {
+  *end = nullptr;
+  if (!c->profiling) return JOFC_OK;
+  if (c->prof_used == c->prof_events.size()) {
+    cudaEvent_t a, b;
+    JOFC_CUDA(cudaEventCreate(&a));
+    JOFC_CUDA(cudaEventCreate(&b));
+    c->prof_events.emplace_back(a, b);
+  }
+  JOFC_CUDA(cudaEventRecord(c->prof_events[c->prof_used].first, c->stream));
+  *end = c->prof_events[c->prof_used].second;
+  ++c->prof_used;
+  return JOFC_OK;
+}
 
 int pass_for_d(jofc_ctx* c, const PassParams& pp) { JOFC_DISPATCH_D(c->d, launch_pass, c, pp); }
 int setup_for_d(jofc_ctx* c) { JOFC_DISPATCH_D(c->d, setup_for, c); }
@@ -364,19 +387,9 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
 
   for (size_t t = 0; t <= max_it; ++t) {
     if (events) JOFC_CUDA(cudaEventRecord((*events)[t], c->stream));
-    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
-    if (c->profiling) {
-      if (c->prof_used == c->prof_events.size()) {
-        cudaEvent_t a, b;
-        JOFC_CUDA(cudaEventCreate(&a));
-        JOFC_CUDA(cudaEventCreate(&b));
-        c->prof_events.emplace_back(a, b);
-      }
-      pe0 = c->prof_events[c->prof_used].first;
-      pe1 = c->prof_events[c->prof_used].second;
-      ++c->prof_used;
-      JOFC_CUDA(cudaEventRecord(pe0, c->stream));
-    }
+    cudaEvent_t pe1 = nullptr;
+    rc = prof_begin(c, &pe1);
+    if (rc) return rc;
     rc = pass_for_d(c, pp);
     if (rc) return rc;
     if (pe1) JOFC_CUDA(cudaEventRecord(pe1, c->stream));
@@ -901,33 +914,64 @@ int jofc_oos_step(jofc_ctx* c, size_t m, size_t n, size_t d, const double* y, co
 // ---------------------------------------------------------------- initialisation
 namespace {
 
+// The panel kernels, instantiated per subspace width p = d + 4.
+struct PanelOps {
+  void (*matvec)(const double*, long long, const double*, double*, int, cudaStream_t);
+  void (*gram_shift)(const double*, const double*, double*, double*, long long, int, double,
+                     double*, int, cudaStream_t);
+  void (*ritz_orth)(double*, const double*, const double*, long long, int,
+                    const init::RitzParams&, double*, double*, int, cudaStream_t);
+  void (*apply_rinv)(double*, long long, const init::RitzParams&, cudaStream_t);
+};
+
 template <int P>
-void launch_matvec(const double* S, long long n, const double* q, double* z, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>((n * 32 + 255) / 256);
-  init::matvec_kernel<P><<<grid, 256, 0, st>>>(S, n, q, z);
+PanelOps panel_ops() {
+  PanelOps o;
+  o.matvec = [](const double* S, long long n, const double* q, double* z, int splits,
+                 cudaStream_t st) {
+    const dim3 grid(static_cast<unsigned>((n + init::kMvRows - 1) / init::kMvRows),
+                    static_cast<unsigned>(splits));
+    init::matvec_sym_kernel<P><<<grid, 256, 0, st>>>(S, n, q, z);
+  };
+  o.gram_shift = [](const double* q, const double* zp, double* z, double* w, long long n,
+                    int splits, double shift, double* part, int grid, cudaStream_t st) {
+    init::gram_shift_kernel<P><<<grid, 256, 0, st>>>(q, zp, z, w, n, splits, shift, part);
+  };
+  o.ritz_orth = [](double* q, const double* z, const double* w, long long n, int k,
+                   const init::RitzParams& prm, double* ritz, double* part, int grid,
+                   cudaStream_t st) {
+    init::ritz_orth_kernel<P><<<grid, 256, 0, st>>>(q, z, w, n, k, prm, ritz, part);
+  };
+  o.apply_rinv = [](double* q, long long n, const init::RitzParams& prm, cudaStream_t st) {
+    init::apply_rinv_kernel<P><<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(q, n, prm);
+  };
+  return o;
 }
 
-int matvec_p(int p, const double* S, long long n, const double* q, double* z, cudaStream_t st) {
+bool panel_ops_for(int p, PanelOps& o) {
   switch (p) {
-    case 5: launch_matvec<5>(S, n, q, z, st); break;
-    case 6: launch_matvec<6>(S, n, q, z, st); break;
-    case 7: launch_matvec<7>(S, n, q, z, st); break;
-    case 8: launch_matvec<8>(S, n, q, z, st); break;
-    case 9: launch_matvec<9>(S, n, q, z, st); break;
-    case 10: launch_matvec<10>(S, n, q, z, st); break;
-    case 11: launch_matvec<11>(S, n, q, z, st); break;
-    case 12: launch_matvec<12>(S, n, q, z, st); break;
-    case 13: launch_matvec<13>(S, n, q, z, st); break;
-    case 14: launch_matvec<14>(S, n, q, z, st); break;
-    default: return set_error(JOFC_EINVAL, "cmds: subspace width %d unsupported", p);
+    case 5: o = panel_ops<5>(); return true;
+    case 6: o = panel_ops<6>(); return true;
+    case 7: o = panel_ops<7>(); return true;
+    case 8: o = panel_ops<8>(); return true;
+    case 9: o = panel_ops<9>(); return true;
+    case 10: o = panel_ops<10>(); return true;
+    case 11: o = panel_ops<11>(); return true;
+    case 12: o = panel_ops<12>(); return true;
+    case 13: o = panel_ops<13>(); return true;
+    case 14: o = panel_ops<14>(); return true;
+    default: return false;
   }
-  JOFC_CUDA(cudaGetLastError());
-  return JOFC_OK;
 }
 
 // cmds (proj/src/init.cpp:21-42) of modality `which` (< 0: the modality
 // average) of the resident problem; x is n x d row-major.
 int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
+  using clk = std::chrono::steady_clock;
+  const bool trace = std::getenv("JOFC_INIT_TRACE") != nullptr;
+  const auto t_start = clk::now();
+  double t_sync = 0.0;  // seconds spent waiting on the device inside the sweep loop
+  int sweeps = 0;
   const Layout& L = c->lay;
   const long long n = L.n;
   if (d < 1 || static_cast<long long>(d) > n)
@@ -997,30 +1041,73 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
     // shifted orthogonal iteration with Rayleigh-Ritz (proj/src/linalg.cpp:167-271)
     const size_t p = k + 4;
     const double shift = snorm, tol = 1e-9 * snorm;
-    init::Mat q(n, p), z(n, p);
+    PanelOps ops;
+    if (!panel_ops_for(static_cast<int>(p), ops))
+      return set_error(JOFC_EINVAL, "cmds: subspace width %zu unsupported", p);
+    init::Mat q(n, p);
     init::Normals rng(0x9e3779b97f4a7c15ull);
     for (double& v : q.a) v = rng.next();
     init::orthonormalize(q);
-    DevBuf<double> dq, dz;
-    JOFC_CUDA(dq.ensure(q.a.size()));
-    JOFC_CUDA(dz.ensure(q.a.size()));
-    bool done = false;
-    for (int iter = 0; iter < 5000 && !done; ++iter) {
-      JOFC_CUDA(cudaMemcpyAsync(dq.p, q.a.data(), q.a.size() * sizeof(double),
-                                cudaMemcpyHostToDevice, c->stream));
-      int rc = matvec_p(static_cast<int>(p), S.p, n, dq.p, dz.p, c->stream);
-      if (rc) return rc;
-      ++c->launches;
-      JOFC_CUDA(cudaMemcpyAsync(z.a.data(), dz.p, z.a.size() * sizeof(double),
+    const int grid1 = std::min<int>(c->num_sms * 8, static_cast<int>((n + 63) / 64));
+    const int grid2 = std::min<int>(c->num_sms * 2, static_cast<int>((n + 255) / 256));
+    const int grid = std::max(grid1, grid2);
+    const size_t part1 = 2 * p * p, part2 = p + p * p;
+    // column splits: enough CTAs for ~16 per SM, each split one n x p partial
+    const long long row_blocks = (n + init::kMvRows - 1) / init::kMvRows;
+    const int splits = static_cast<int>(std::min<long long>(
+        init::kMvMaxSplits, std::max<long long>(1, (16LL * c->num_sms + row_blocks - 1) / row_blocks)));
+    DevBuf<double> dq, dzp, dz, dw, dritz, dpart;
+    JOFC_CUDA(dzp.ensure(splits * n * p));
+    JOFC_CUDA(dq.ensure(n * p));
+    JOFC_CUDA(dz.ensure(n * p));
+    JOFC_CUDA(dw.ensure(n * p));
+    JOFC_CUDA(dritz.ensure(n * k));
+    JOFC_CUDA(dpart.ensure(grid * std::max(part1, part2)));
+    // pinned staging for the per-CTA partials (two small D2H reads per sweep)
+    struct Pinned {
+      double* p = nullptr;
+      ~Pinned() {
+        if (p) cudaFreeHost(p);
+      }
+    } hpart;
+    JOFC_CUDA(cudaMallocHost(&hpart.p, grid * std::max(part1, part2) * sizeof(double)));
+    JOFC_CUDA(cudaMemcpyAsync(dq.p, q.a.data(), q.a.size() * sizeof(double),
+                              cudaMemcpyHostToDevice, c->stream));
+    auto fetch = [&](int blocks, size_t per) -> int {
+      JOFC_CUDA(cudaGetLastError());
+      const auto t0 = clk::now();
+      JOFC_CUDA(cudaMemcpyAsync(hpart.p, dpart.p, blocks * per * sizeof(double),
                                 cudaMemcpyDeviceToHost, c->stream));
       JOFC_CUDA(cudaStreamSynchronize(c->stream));
-      init::Mat t(p, p);
-      for (size_t i = 0; i < p; ++i)
-        for (size_t j = 0; j < p; ++j) {
-          double dot = 0.0;
-          for (long long r = 0; r < n; ++r) dot += q(r, i) * z(r, j);
-          t(i, j) = dot;
-        }
+      t_sync += std::chrono::duration<double>(clk::now() - t0).count();
+      return JOFC_OK;
+    };
+    auto sum_part = [&](int blocks, size_t per, size_t off, size_t cnt, std::vector<double>& out) {
+      out.assign(cnt, 0.0);
+      for (int b = 0; b < blocks; ++b)
+        for (size_t e = 0; e < cnt; ++e) out[e] += hpart.p[b * per + off + e];
+    };
+    bool done = false;
+    std::vector<double> acc;
+    if (trace)
+      std::fprintf(stderr, "[init] cmds(%d) n=%lld p=%zu setup %.3f s\n", which, n, p,
+                   std::chrono::duration<double>(clk::now() - t_start).count());
+    for (int iter = 0; iter < 5000 && !done; ++iter) {
+      ++sweeps;
+      cudaEvent_t pe1 = nullptr;
+      int rc = prof_begin(c, &pe1);
+      if (rc) return rc;
+      ops.matvec(S.p, n, dq.p, dzp.p, splits, c->stream);
+      if (pe1) JOFC_CUDA(cudaEventRecord(pe1, c->stream));
+      ops.gram_shift(dq.p, dzp.p, dz.p, dw.p, n, splits, shift, dpart.p, grid1, c->stream);
+      c->launches += 2;
+      rc = fetch(grid1, part1);
+      if (rc) return rc;
+      init::Mat t(p, p), g(p, p);
+      sum_part(grid1, part1, 0, p * p, acc);
+      std::copy(acc.begin(), acc.end(), t.a.begin());
+      sum_part(grid1, part1, p * p, p * p, acc);
+      std::copy(acc.begin(), acc.end(), g.a.begin());
       for (size_t i = 0; i < p; ++i)
         for (size_t j = i + 1; j < p; ++j) t(i, j) = t(j, i) = 0.5 * (t(i, j) + t(j, i));
       std::vector<double> theta;
@@ -1031,25 +1118,30 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
       std::iota(order.begin(), order.end(), size_t{0});
       std::stable_sort(order.begin(), order.end(),
                        [&](size_t a, size_t b) { return theta[a] > theta[b]; });
-      bool conv = true;
-      init::Mat ritz(n, k);
-      for (size_t cc = 0; cc < k && conv; ++cc) {
-        const size_t col = order[cc];
-        double res2 = 0.0;
-        for (long long r = 0; r < n; ++r) {
-          double rv = 0.0, zv = 0.0;
-          for (size_t j = 0; j < p; ++j) {
-            rv += q(r, j) * u(j, col);
-            zv += z(r, j) * u(j, col);
-          }
-          ritz(r, cc) = rv;
-          const double df = zv - theta[col] * rv;
-          res2 += df * df;
-        }
-        values[cc] = theta[col];
-        if (std::sqrt(res2) > tol) conv = false;
+      init::RitzParams prm{};
+      for (size_t cc = 0; cc < k; ++cc) {
+        for (size_t j = 0; j < p; ++j) prm.u[j * init::kMaxP + cc] = u(j, order[cc]);
+        prm.theta[cc] = theta[order[cc]];
+        values[cc] = theta[order[cc]];
       }
+      init::Mat rinv;
+      const bool chol = init::cholesky_rinv(g, rinv);
+      for (size_t i = 0; i < p; ++i)
+        for (size_t j = 0; j < p; ++j)
+          prm.rinv[i * init::kMaxP + j] = chol ? rinv(i, j) : (i == j ? 1.0 : 0.0);
+      ops.ritz_orth(dq.p, dz.p, dw.p, n, static_cast<int>(k), prm, dritz.p, dpart.p, grid2,
+                    c->stream);
+      ++c->launches;
+      rc = fetch(grid2, part2);
+      if (rc) return rc;
+      sum_part(grid2, part2, 0, k, acc);
+      bool conv = true;
+      for (size_t cc = 0; cc < k; ++cc)
+        if (std::sqrt(acc[cc]) > tol) conv = false;
       if (conv) {
+        init::Mat ritz(n, k);
+        JOFC_CUDA(cudaMemcpy(ritz.a.data(), dritz.p, ritz.a.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost));
         for (size_t cc = 0; cc < k; ++cc) {
           std::vector<double> col(n);
           double nr = 0.0;
@@ -1065,14 +1157,37 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
         done = true;
         break;
       }
-      for (size_t i = 0; i < z.a.size(); ++i) z.a[i] += shift * q.a[i];
-      q = z;
-      init::orthonormalize(q);
+      if (!chol) {  // ill-conditioned panel: the reference's Gram-Schmidt on the host
+        JOFC_CUDA(cudaMemcpy(q.a.data(), dw.p, q.a.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+        init::orthonormalize(q);
+        JOFC_CUDA(cudaMemcpy(dq.p, q.a.data(), q.a.size() * sizeof(double),
+                             cudaMemcpyHostToDevice));
+        continue;
+      }
+      sum_part(grid2, part2, p, p * p, acc);
+      std::copy(acc.begin(), acc.end(), g.a.begin());
+      if (init::cholesky_rinv(g, rinv)) {
+        for (size_t i = 0; i < p; ++i)
+          for (size_t j = 0; j < p; ++j) prm.rinv[i * init::kMaxP + j] = rinv(i, j);
+        ops.apply_rinv(dq.p, n, prm, c->stream);
+        ++c->launches;
+        JOFC_CUDA(cudaGetLastError());
+      } else {
+        JOFC_CUDA(cudaMemcpy(q.a.data(), dq.p, q.a.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+        init::orthonormalize(q);
+        JOFC_CUDA(cudaMemcpy(dq.p, q.a.data(), q.a.size() * sizeof(double),
+                             cudaMemcpyHostToDevice));
+      }
     }
     if (!done)
       return set_error(JOFC_ENUMERIC,
                        "subspace eigensolver did not converge within the iteration cap");
   }
+  if (trace)
+    std::fprintf(stderr, "[init] cmds(%d) total %.3f s, %d sweeps, device wait %.3f s\n", which,
+                 std::chrono::duration<double>(clk::now() - t_start).count(), sweeps, t_sync);
   x = init::Mat(n, d);
   for (size_t cc = 0; cc < d; ++cc) {
     const double sc = std::sqrt(std::max(values[cc], 0.0));  // Torgerson clamp

@@ -55,3 +55,29 @@ def test_default_init_solve_matches_reference(R):
     assert got.iterations == ref.iterations
     assert rel_fro(got.config, ref.x) < 1e-8
     assert max(abs(a - b) / abs(b) for a, b in zip(got.stress_trace, ref.trace)) < 1e-10
+
+
+@pytest.mark.parametrize("d", [5, 10])
+def test_cmds_average_wide_panel(R, d):
+    # the modality average (as averaged_procrustes_init builds it) and the
+    # widest panels p = d + 4 up to 14
+    delta = problem(700, m=3, seed=5, p=12)
+    prob = jg.OmnibusProblem(list(delta), validate=False)
+    ref = R.cmds(delta, -1, d)
+    got = jg.cmds(prob, -1, d)
+    assert rel_fro(got, ref) < 1e-7, rel_fro(got, ref)
+
+
+def test_cmds_low_rank(R):
+    # collinear objects: S has rank 1, the trailing eigenpairs are degenerate
+    # (null space) and clamp to zero columns
+    P = Port()
+    rng = np.random.default_rng(21)
+    t = rng.normal(size=(400, 1))
+    feats = np.hstack([t, 2.0 * t])
+    delta = np.stack([P.distance_matrix(feats), P.distance_matrix(1.5 * feats)])
+    prob = jg.OmnibusProblem(list(delta), validate=False)
+    for modality in (0, -1):
+        ref = R.cmds(delta, modality, 3)
+        got = jg.cmds(prob, modality, 3)
+        assert rel_fro(got, ref) < 1e-7, (modality, rel_fro(got, ref))
