@@ -76,7 +76,7 @@ int jofc_set_allreduce(jofc_ctx* ctx, jofc_allreduce_fn fn, void* user);
 
 /* OmnibusProblem upload (proj/include/jofc/problem.hpp:16-34): m dense n x n
  * dissimilarities, delta[l] -> n*n row-major.  Only the upper triangle is
- * read; it is packed into HBM-resident 64x64 tiles and checked finite and
+ * read; it is packed into HBM-resident 128x64 blocks and checked finite and
  * nonnegative.  normalize != 0 divides each modality by its Frobenius norm
  * first (OmnibusProblem::normalized, proj/src/problem.cpp:34-42). */
 int jofc_set_problem(jofc_ctx* ctx, size_t m, size_t n, const double* const* delta,
@@ -86,6 +86,18 @@ int jofc_set_problem(jofc_ctx* ctx, size_t m, size_t n, const double* const* del
  * (proj/src/distance.cpp:8-29), written straight into the packed layout. */
 int jofc_set_problem_features(jofc_ctx* ctx, size_t m, size_t n, size_t p,
                               const double* features);
+/* load_dissimilarities (proj/include/jofc/io.hpp:19-23, proj/src/io.cpp:152-215)
+ * streamed from files straight into the packed layout, no host n x n copy:
+ * one headerless CSV per modality, or a single ".jofc" problem file
+ * (proj/src/io.cpp:84-125).  Same validation, order and messages as the
+ * reference (symmetry averaged within 1e-9 relative, nonzero diagonals warned
+ * on stderr and dropped, negative / non-finite entries rejected naming file
+ * and index), then OmnibusProblem's checks.  normalize != 0 divides each
+ * modality by its Frobenius norm (device reduction; unsharded contexts). */
+int jofc_load_problem_files(jofc_ctx* ctx, size_t count, const char* const* paths,
+                            int normalize);
+/* Shape (m, n) of the resident problem. */
+int jofc_problem_shape(jofc_ctx* ctx, size_t* m, size_t* n);
 /* Bytes of packed Delta resident on this context (its shard only). */
 size_t jofc_problem_bytes(jofc_ctx* ctx);
 /* Number of packed pairs m*n(n-1)/2 (all shards). */

@@ -294,6 +294,30 @@ class Reference:
         self._cache[key] = (h, delta)
         return h
 
+    def load_dissimilarities(self, paths):
+        """proj/src/io.cpp:152-215 -> dense (m, n, n) array (raises on error)."""
+        L = self.lib
+        L.ref_load_dissimilarities.restype = C.c_void_p
+        L.ref_load_dissimilarities.argtypes = [C.POINTER(C.c_char_p), _sz]
+        enc = [os.fsencode(p) for p in paths]
+        h = L.ref_load_dissimilarities((C.c_char_p * len(enc))(*enc), _sz(len(enc)))
+        if not h:
+            _raise(1, L.ref_last_error().decode())
+        h = C.c_void_p(h)
+        try:
+            m, n = _sz(), _sz()
+            L.ref_problem_shape(h, C.byref(m), C.byref(n))
+            out = np.empty((m.value, n.value, n.value))
+            for l in range(m.value):
+                self._check(L.ref_problem_modality(h, _sz(l), _ptr(out[l])))
+            return out
+        finally:
+            L.ref_problem_destroy(h)
+
+    def save_problem_binary(self, delta, path):
+        """proj/src/io.cpp:217-223 (the reference's own .jofc writer)."""
+        self._check(self.lib.ref_save_problem_binary(self.problem(delta), os.fsencode(path)))
+
     def release(self):
         for h, _ in self._cache.values():
             self.lib.ref_problem_destroy(h)

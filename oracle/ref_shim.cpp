@@ -18,6 +18,7 @@
 
 #include "jofc/distance.hpp"
 #include "jofc/init.hpp"
+#include "jofc/io.hpp"
 #include "jofc/linalg.hpp"
 #include "jofc/oos.hpp"
 #include "jofc/problem.hpp"
@@ -169,6 +170,35 @@ void* ref_problem_create(size_t m, size_t n, const double* delta) {
 }
 
 void ref_problem_destroy(void* p) { delete static_cast<OmnibusProblem*>(p); }
+
+// load_dissimilarities (proj/src/io.cpp:152-215): a problem handle, or null
+// with ref_last_error() set.
+void* ref_load_dissimilarities(const char* const* paths, size_t count) {
+  OmnibusProblem* out = nullptr;
+  int rc = guarded([&] {
+    std::vector<std::string> ps(paths, paths + count);
+    out = new OmnibusProblem(load_dissimilarities(ps));
+  });
+  return rc ? nullptr : out;
+}
+
+int ref_problem_shape(void* prob, size_t* m, size_t* n) {
+  const auto& p = *static_cast<OmnibusProblem*>(prob);
+  *m = p.modality_count();
+  *n = p.object_count();
+  return 0;
+}
+
+int ref_problem_modality(void* prob, size_t l, double* out) {
+  return guarded([&] {
+    const auto& d = static_cast<OmnibusProblem*>(prob)->modality(l);
+    std::memcpy(out, d.data(), d.size() * sizeof(double));
+  });
+}
+
+int ref_save_problem_binary(void* prob, const char* path) {
+  return guarded([&] { save_problem_binary(path, *static_cast<OmnibusProblem*>(prob)); });
+}
 
 int ref_raw_stress(void* prob, const jo_weights* spec, size_t d, const double* x, int parallel,
                    double* out) {

@@ -11,6 +11,7 @@ from .api import (  # noqa: F401
     OmnibusProblem,
     OosOptions,
     OosResult,
+    ResidentProblem,
     SolveOptions,
     Termination,
     WeightSpec,
@@ -19,6 +20,7 @@ from .api import (  # noqa: F401
     default_device,
     fjofc_embed,
     guttman_step_fast,
+    load_dissimilarities,
     oos_embed,
     oos_embed_batch,
     oos_start,

@@ -67,6 +67,8 @@ _SIGS = {
     "jofc_set_allreduce": (C.c_int, [_vp, ALLREDUCE_FN, _vp]),
     "jofc_set_problem": (C.c_int, [_vp, _sz, _sz, C.POINTER(_dp), C.c_int]),
     "jofc_set_problem_features": (C.c_int, [_vp, _sz, _sz, _sz, _dp]),
+    "jofc_load_problem_files": (C.c_int, [_vp, _sz, C.POINTER(C.c_char_p), C.c_int]),
+    "jofc_problem_shape": (C.c_int, [_vp, _szp, _szp]),
     "jofc_problem_bytes": (_sz, [_vp]),
     "jofc_problem_pairs": (C.c_double, [_vp]),
     "jofc_raw_stress": (C.c_int, [_vp, C.POINTER(Weights), _sz, _dp, _dp]),

@@ -31,6 +31,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Optional
@@ -159,6 +160,31 @@ class OmnibusProblem:
         return OmnibusProblem([d[:count, :count] for d in self.modalities], validate=False)
 
 
+class ResidentProblem:
+    """A problem that lives only in HBM: loaded by load_dissimilarities straight
+    from files into one Device's packed layout (no host n x n copy).  Usable
+    wherever an OmnibusProblem is accepted, with that device."""
+
+    def __init__(self, device, m, n, key):
+        self.device, self._m, self._n, self._key = device, m, n, key
+
+    def modality_count(self):
+        return self._m
+
+    def object_count(self):
+        return self._n
+
+
+def load_dissimilarities(paths, device=None, normalize=False):
+    """proj/include/jofc/io.hpp:19-23 (load_dissimilarities), streamed on the
+    device: one CSV per modality or a single .jofc problem file.  Returns a
+    ResidentProblem bound to `device` (default device 0)."""
+    dev = device or default_device()
+    if isinstance(paths, (str, bytes)):
+        paths = [paths]
+    return dev.load_files(list(paths), normalize=normalize)
+
+
 def stress_pair_count(m, n):
     mn = float(m) * float(n)
     return mn * (mn - 1.0) / 2.0
@@ -262,7 +288,28 @@ class Device:
         self._hook = _capi.ALLREDUCE_FN(tramp)
         check(self.lib.jofc_set_allreduce(self.h, self._hook, None))
 
-    def upload(self, problem: OmnibusProblem, normalize=False):
+    def load_files(self, paths, normalize=False):
+        enc = [os.fsencode(p) for p in paths]
+        arr = (C.c_char_p * len(enc))(*enc)
+        check(self.lib.jofc_load_problem_files(self.h, len(enc), arr, int(bool(normalize))))
+        key = ("files", tuple(paths), bool(normalize), object())
+        self._problem_key = key
+        self._keep = None
+        m, n = self._resident_shape()
+        return ResidentProblem(self, m, n, key)
+
+    def _resident_shape(self):
+        m, n = C.c_size_t(), C.c_size_t()
+        check(self.lib.jofc_problem_shape(self.h, C.byref(m), C.byref(n)))
+        return m.value, n.value
+
+    def upload(self, problem, normalize=False):
+        if isinstance(problem, ResidentProblem):
+            if problem.device is not self or problem._key != self._problem_key:
+                raise InvalidArgument("ResidentProblem: no longer resident on this device")
+            if normalize:
+                raise InvalidArgument("ResidentProblem: load with normalize=True instead")
+            return
         key = (id(problem), problem._version, bool(normalize))
         if key == self._problem_key:
             return
