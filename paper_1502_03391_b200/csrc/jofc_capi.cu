@@ -10,6 +10,8 @@
 // decrease < eps rule, proj/src/solver.cpp:138-143) is decided on the device
 // and later launches exit at entry once the control block says done.
 #include <cuda_runtime.h>
+#include <omp.h>
+#include <unistd.h>
 
 #include <chrono>
 
@@ -81,6 +83,40 @@ struct DevBuf {
   }
 };
 
+// Double-buffered staging of streaming ingest (kept across loads): pinned
+// host panels, their copy-done events, and the device panels.
+struct IngestPanels {
+  double* host[2] = {nullptr, nullptr};
+  size_t cap = 0;  // doubles per panel
+  cudaEvent_t copied[2] = {nullptr, nullptr};
+  DevBuf<double> stage[2];
+  void release() {
+    for (int k = 0; k < 2; ++k) {
+      if (host[k]) cudaFreeHost(host[k]);
+      if (copied[k]) cudaEventDestroy(copied[k]);
+      host[k] = nullptr;
+      copied[k] = nullptr;
+      stage[k].release();
+    }
+    cap = 0;
+  }
+  cudaError_t ensure(size_t doubles) {
+    if (doubles <= cap) return cudaSuccess;
+    release();
+    for (int k = 0; k < 2; ++k) {
+      cudaError_t e = cudaMallocHost(&host[k], doubles * sizeof(double));
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = stage[k].ensure(doubles);
+      if (e != cudaSuccess) {
+        release();
+        return e;
+      }
+    }
+    cap = doubles;
+    return cudaSuccess;
+  }
+};
+
 }  // namespace
 
 struct jofc_ctx {
@@ -115,6 +151,8 @@ struct jofc_ctx {
   // oos state
   DevBuf<double> oos_x, oos_delta, oos_y0, oos_y1, oos_part, oos_trace;
   DevBuf<OosPoint> oos_st;
+  // streaming ingest staging
+  IngestPanels ingest;
 };
 
 namespace {
@@ -473,6 +511,7 @@ int jofc_ctx_destroy(jofc_ctx* c) {
   }
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   if (c->ctrl_host) cudaFreeHost(c->ctrl_host);
+  c->ingest.release();
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return JOFC_OK;
@@ -1269,17 +1308,6 @@ struct InputCheck {
   std::vector<std::pair<long long, double>> diag;  // nonzero diagonal entries
 };
 
-struct PinnedPanels {
-  double* host[2] = {nullptr, nullptr};
-  cudaEvent_t copied[2] = {nullptr, nullptr};
-  ~PinnedPanels() {
-    for (int k = 0; k < 2; ++k) {
-      if (host[k]) cudaFreeHost(host[k]);
-      if (copied[k]) cudaEventDestroy(copied[k]);
-    }
-  }
-};
-
 void check_row(InputCheck& ck, long long r, const double* v, long long cols) {
   if (!ck.bad)
     for (long long j = 0; j < cols; ++j) {
@@ -1331,59 +1359,62 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
   const bool device = m >= 1 && n >= 2;
   if (normalize && c->world > 1)
     return set_error(JOFC_EINVAL, "load with normalize needs an unsharded context");
-  DevBuf<double> stage[2];
+  // panels of whole row blocks, ~64 MB each
+  const long long panel_rows =
+      std::max<long long>(1, (64LL << 20) / (8LL * std::max<long long>(n, 1)) / kRows) * kRows;
   DevBuf<unsigned long long> keys;
-  PinnedPanels pin;
+  IngestPanels& pin = c->ingest;
   if (device) {
     make_layout(c, static_cast<size_t>(m), static_cast<size_t>(n));
     JOFC_CUDA(c->delta.ensure(static_cast<size_t>(std::max<long long>(c->lay.local(), 1)) *
                               kBlockElems));
-    for (int k = 0; k < 2; ++k) {
-      JOFC_CUDA(stage[k].ensure(static_cast<size_t>(kRows) * n));
-      JOFC_CUDA(cudaMallocHost(&pin.host[k], static_cast<size_t>(kRows) * n * sizeof(double)));
-      JOFC_CUDA(cudaEventCreateWithFlags(&pin.copied[k], cudaEventDisableTiming));
-    }
+    JOFC_CUDA(pin.ensure(static_cast<size_t>(panel_rows) * n));
     JOFC_CUDA(keys.ensure(static_cast<size_t>(m)));
     JOFC_CUDA(cudaMemsetAsync(keys.p, 0xff, m * sizeof(unsigned long long), c->stream));
   }
   const Layout& L = c->lay;
   long long panels = 0;
-  // ships host panel k (row block B of modality l, `rows` rows) to the device
-  auto flush = [&](int k, int l, int B, int rows) -> int {
-    JOFC_CUDA(cudaMemcpyAsync(stage[k].p, pin.host[k], static_cast<size_t>(rows) * n * sizeof(double),
+  // ships host panel k (rows [r0, r0 + rows) of modality l; r0 a multiple of
+  // 128) to the device and packs it row block by row block
+  auto flush = [&](int k, int l, long long r0, long long rows) -> int {
+    JOFC_CUDA(cudaMemcpyAsync(pin.stage[k].p, pin.host[k], static_cast<size_t>(rows) * n * sizeof(double),
                               cudaMemcpyHostToDevice, c->stream));
     JOFC_CUDA(cudaEventRecord(pin.copied[k], c->stream));
-    PackParams pk{};
-    pk.stage = stage[k].p;
-    pk.pitch = n;
-    pk.r0 = static_cast<long long>(B) * kRows;
-    pk.c0 = 0;
-    pk.n = n;
-    pk.nT = L.nT;
-    pk.bpm = L.bpm;
-    pk.g_first = static_cast<long long>(l) * L.bpm + row_first(L.nT, B);
-    pk.begin = L.begin;
-    pk.end = L.end;
-    pk.dst = c->delta.p;
-    pk.norm = 0.0;
-    pk.bad = nullptr;
-    jofc_pack_kernel<<<static_cast<unsigned>(L.nT - 2 * B), 256, 0, c->stream>>>(pk);
-    JOFC_CUDA(cudaGetLastError());
-    CombineParams cb{};
-    cb.stage = stage[k].p;
-    cb.n = n;
-    cb.nT = L.nT;
-    cb.bpm = L.bpm;
-    cb.l = l;
-    cb.Bp = B;
-    cb.rows = rows;
-    cb.begin = L.begin;
-    cb.end = L.end;
-    cb.dst = c->delta.p;
-    cb.asym_key = keys.p + l;
-    jofc_ingest_combine_kernel<<<static_cast<unsigned>(2 * (B + 1)), 256, 0, c->stream>>>(cb);
-    JOFC_CUDA(cudaGetLastError());
-    c->launches += 2;
+    for (long long rb = r0; rb < r0 + rows; rb += kRows) {
+      const int B = static_cast<int>(rb / kRows);
+      const double* st = pin.stage[k].p + (rb - r0) * n;
+      PackParams pk{};
+      pk.stage = st;
+      pk.pitch = n;
+      pk.r0 = rb;
+      pk.c0 = 0;
+      pk.n = n;
+      pk.nT = L.nT;
+      pk.bpm = L.bpm;
+      pk.g_first = static_cast<long long>(l) * L.bpm + row_first(L.nT, B);
+      pk.begin = L.begin;
+      pk.end = L.end;
+      pk.dst = c->delta.p;
+      pk.norm = 0.0;
+      pk.bad = nullptr;
+      jofc_pack_kernel<<<static_cast<unsigned>(L.nT - 2 * B), 256, 0, c->stream>>>(pk);
+      JOFC_CUDA(cudaGetLastError());
+      CombineParams cb{};
+      cb.stage = st;
+      cb.n = n;
+      cb.nT = L.nT;
+      cb.bpm = L.bpm;
+      cb.l = l;
+      cb.Bp = B;
+      cb.rows = static_cast<int>(std::min<long long>(kRows, r0 + rows - rb));
+      cb.begin = L.begin;
+      cb.end = L.end;
+      cb.dst = c->delta.p;
+      cb.asym_key = keys.p + l;
+      jofc_ingest_combine_kernel<<<static_cast<unsigned>(2 * (B + 1)), 256, 0, c->stream>>>(cb);
+      JOFC_CUDA(cudaGetLastError());
+      c->launches += 2;
+    }
     return JOFC_OK;
   };
   auto acquire = [&](int k) -> int {  // host panel k free again (its last copy landed)
@@ -1397,23 +1428,55 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
     ck.name = binary ? p0 : paths[l];
     if (binary) {
       ck.rows = ck.cols = n;
-      for (long long r0 = 0; r0 < n; r0 += kRows) {
-        const int rows = static_cast<int>(std::min<long long>(kRows, n - r0));
+      const int fd = fileno(bf);
+      std::vector<double> scratch;
+      for (long long r0 = 0; r0 < n; r0 += panel_rows) {
+        const long long rows = std::min<long long>(panel_rows, n - r0);
         const int k = static_cast<int>(panels & 1);
         int rc = acquire(k);
         if (rc) return rc;
-        double* dst = device ? pin.host[k] : nullptr;
-        std::vector<double> scratch;
-        if (!dst) {
+        double* dst = pin.host[k];
+        if (!device) {
           scratch.resize(static_cast<size_t>(rows) * n);
           dst = scratch.data();
         }
-        if (std::fread(dst, sizeof(double), static_cast<size_t>(rows) * n, bf) !=
-            static_cast<size_t>(rows) * n)
-          return set_error(JOFC_EINVAL, "'%s': truncated payload", p0.c_str());
-        for (int i = 0; i < rows; ++i) check_row(ck, r0 + i, dst + static_cast<size_t>(i) * n, n);
+        // parallel positioned reads + entry checks, one slab of rows per thread
+        const int nt = std::max(1, std::min(16, omp_get_max_threads()));
+        std::vector<InputCheck> part(nt);
+        int io_err = 0;
+#pragma omp parallel num_threads(nt)
+        {
+          const int t = omp_get_thread_num();
+          const long long a = rows * t / nt, b = rows * (t + 1) / nt;
+          const size_t bytes = static_cast<size_t>(b - a) * n * sizeof(double);
+          const off_t off = 20 + static_cast<off_t>((l * n + r0 + a) * n) * 8;
+          size_t done = 0;
+          while (done < bytes) {
+            const ssize_t got = pread(fd, reinterpret_cast<char*>(dst + (a * n)) + done,
+                                      bytes - done, off + static_cast<off_t>(done));
+            if (got <= 0) {
+#pragma omp atomic write
+              io_err = 1;
+              break;
+            }
+            done += static_cast<size_t>(got);
+          }
+          if (done == bytes)
+            for (long long i = a; i < b; ++i) check_row(part[t], r0 + i, dst + i * n, n);
+        }
+        if (io_err) return set_error(JOFC_EINVAL, "'%s': truncated payload", p0.c_str());
+        for (const InputCheck& pc : part) {  // merge in row order
+          if (pc.bad && !ck.bad) {
+            ck.bad = true;
+            ck.nonfinite = pc.nonfinite;
+            ck.bi = pc.bi;
+            ck.bj = pc.bj;
+            ck.bv = pc.bv;
+          }
+          ck.diag.insert(ck.diag.end(), pc.diag.begin(), pc.diag.end());
+        }
         if (device && !ck.bad) {
-          rc = flush(k, static_cast<int>(l), static_cast<int>(r0 / kRows), rows);
+          rc = flush(k, static_cast<int>(l), r0, rows);
           if (rc) return rc;
           ++panels;
         }
@@ -1430,7 +1493,7 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
     }
     ck.cols = static_cast<long long>(row.size());
     const bool packable = device && ck.cols == n;
-    int filled = 0;
+    long long filled = 0;
     int k = static_cast<int>(panels & 1);
     bool have = true;
     for (long long r = 0;; ++r) {
@@ -1452,8 +1515,8 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
           if (rc) return rc;
         }
         std::memcpy(pin.host[k] + static_cast<size_t>(filled) * n, row.data(), n * sizeof(double));
-        if (++filled == kRows || r == n - 1) {
-          const int rc = flush(k, static_cast<int>(l), static_cast<int>(r / kRows), filled);
+        if (++filled == panel_rows || r == n - 1) {
+          const int rc = flush(k, static_cast<int>(l), r + 1 - filled, filled);
           if (rc) return rc;
           ++panels;
           filled = 0;
