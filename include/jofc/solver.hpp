@@ -11,8 +11,8 @@ namespace jofc {
 Configuration guttman_step_fast(const Configuration& config, const OmnibusProblem& problem,
                                 const WeightSpec& spec, bool parallel = false);
 
-// InitKind::provided and InitKind::averaged_procrustes (the default; cMDS +
-// Procrustes on the GPU).  InitKind::imputed_cmds throws std::invalid_argument.
+// Every InitKind: provided, averaged_procrustes (the default) and imputed_cmds,
+// the latter two computed on the GPU from the resident Delta.
 EmbeddingResult fjofc_embed(const OmnibusProblem& problem, const WeightSpec& spec,
                             const SolveOptions& options);
 

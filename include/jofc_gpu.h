@@ -159,6 +159,11 @@ int jofc_oos_batch(jofc_ctx* ctx, size_t k, size_t m, size_t n, size_t d, const 
  * reference's default InitKind. */
 int jofc_cmds(jofc_ctx* ctx, int modality, size_t d, double* x_out);
 int jofc_init_averaged_procrustes(jofc_ctx* ctx, size_t d, double* x_out);
+/* imputed_omnibus_init (proj/src/init.cpp:90-116): cmds of the m n x m n
+ * omnibus matrix (off-diagonal blocks (Delta_i + Delta_j) / 2), split into
+ * modality blocks, each re-centred.  Rejects m n > dense_cap like the
+ * reference. */
+int jofc_init_imputed_cmds(jofc_ctx* ctx, size_t d, size_t dense_cap, double* x_out);
 
 #ifdef __cplusplus
 }

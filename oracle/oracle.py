@@ -395,6 +395,13 @@ class Reference:
         self._check(self.lib.ref_cmds(self.problem(delta), int(modality), _sz(d), _ptr(out)))
         return out
 
+    def imputed_omnibus_init(self, delta, d, dense_cap=4096):
+        m, n, _ = delta.shape
+        out = np.empty((m, n, d))
+        self._check(self.lib.ref_imputed_omnibus_init(self.problem(delta), _sz(d), _sz(dense_cap),
+                                                      _ptr(out)))
+        return out
+
     def averaged_procrustes_init(self, delta, d):
         m, n, _ = delta.shape
         out = np.empty((m, n, d))

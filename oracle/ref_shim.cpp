@@ -280,6 +280,13 @@ int ref_cmds(void* prob, int modality, size_t d, double* x_out) {
   });
 }
 
+int ref_imputed_omnibus_init(void* prob, size_t d, size_t dense_cap, double* x_out) {
+  return guarded([&] {
+    const auto& p = *static_cast<OmnibusProblem*>(prob);
+    from_config(imputed_omnibus_init(p, d, dense_cap), x_out);
+  });
+}
+
 int ref_averaged_procrustes_init(void* prob, size_t d, int parallel, double* x_out) {
   return guarded([&] {
     const auto& p = *static_cast<OmnibusProblem*>(prob);

@@ -20,6 +20,7 @@ from .api import (  # noqa: F401
     default_device,
     fjofc_embed,
     guttman_step_fast,
+    imputed_omnibus_init,
     load_dissimilarities,
     oos_embed,
     oos_embed_batch,

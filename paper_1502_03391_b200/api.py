@@ -396,11 +396,20 @@ def averaged_procrustes_init(problem, d, normalize=False, device=None):
     return out
 
 
+def imputed_omnibus_init(problem, d, dense_cap=4096, normalize=False, device=None):
+    """proj/src/init.cpp:90-116 on the GPU (cmds of the imputed omnibus matrix)."""
+    dev = device or default_device()
+    dev.upload(problem, normalize=normalize)
+    out = np.empty((problem.modality_count(), problem.object_count(), int(d)))
+    check(dev.lib.jofc_init_imputed_cmds(dev.h, int(d), int(dense_cap), dptr(out)))
+    return out
+
+
 def fjofc_embed(problem, spec, options: SolveOptions, device=None):
     """proj/src/solver.cpp:223-236 (+ run_majorization :106-150) on the GPU.
 
-    InitKind.provided and InitKind.averaged_procrustes (the default, computed on
-    the GPU); InitKind.imputed_cmds is not built."""
+    Every InitKind: provided, averaged_procrustes (the default) and
+    imputed_cmds, the latter two computed on the GPU."""
     if options.dim < 1:
         raise InvalidArgument("SolveOptions: dim must be positive")
     if not options.eps > 0:
@@ -417,7 +426,8 @@ def fjofc_embed(problem, spec, options: SolveOptions, device=None):
     elif options.init == InitKind.averaged_procrustes:
         x0 = averaged_procrustes_init(problem, options.dim, options.normalize, device=dev)
     else:
-        raise NotImplementedError("InitKind.imputed_cmds is not built on the GPU path")
+        x0 = imputed_omnibus_init(problem, options.dim, options.dense_cap, options.normalize,
+                                  device=dev)
     T = int(options.max_iterations)
     x = np.empty_like(x0)
     trace = np.empty(T + 1)

@@ -119,8 +119,17 @@ Configuration averaged_procrustes_init(const OmnibusProblem& problem, std::size_
   return unflatten(x, problem.modality_count(), problem.object_count(), d);
 }
 
+Configuration imputed_omnibus_init(const OmnibusProblem& problem, std::size_t d,
+                                   std::size_t dense_cap) {
+  Ctx& c = with_problem(problem, false);
+  std::vector<double> x(problem.modality_count() * problem.object_count() * d);
+  check(jofc_init_imputed_cmds(c.h, d, dense_cap, x.data()));
+  return unflatten(x, problem.modality_count(), problem.object_count(), d);
+}
+
 DenseMatrix cmds(const DenseMatrix& delta, std::size_t d) {
-  // one-modality problem, its own (short-lived) residency
+  if (!is_square(delta)) throw std::invalid_argument("cmds: matrix not square");
+  // one-modality problem (its upper triangle), its own short-lived residency
   OmnibusProblem single({delta});
   Ctx& c = with_problem(single, false);
   DenseMatrix out(delta.rows(), d);
@@ -182,9 +191,10 @@ EmbeddingResult fjofc_embed(const OmnibusProblem& problem, const WeightSpec& spe
     check(jofc_init_averaged_procrustes(c.h, d, x.data()));
     start = unflatten(x, m, n, d);
   } else if (options.init == InitKind::imputed_cmds) {
-    throw std::invalid_argument(
-        "fjofc_embed: InitKind::imputed_cmds is not part of this build (use "
-        "averaged_procrustes or provided)");
+    Ctx& c = with_problem(problem, options.normalize);
+    std::vector<double> x(m * n * d);
+    check(jofc_init_imputed_cmds(c.h, d, options.dense_cap, x.data()));
+    start = unflatten(x, m, n, d);
   } else {
     if (!options.init_config)
       throw std::invalid_argument("SolveOptions: provided init missing a configuration");

@@ -1005,8 +1005,11 @@ bool panel_ops_for(int p, PanelOps& o) {
   }
 }
 
-// cmds (proj/src/init.cpp:21-42) of modality `which` (< 0: the modality
-// average) of the resident problem; x is n x d row-major.
+constexpr int kOmnibus = -2;
+
+// cmds (proj/src/init.cpp:21-42) of modality `which` (-1: the modality
+// average, kOmnibus: the imputed omnibus matrix) of the resident problem; x is
+// n x d (m n x d for the omnibus) row-major.
 int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
   using clk = std::chrono::steady_clock;
   const bool trace = std::getenv("JOFC_INIT_TRACE") != nullptr;
@@ -1014,15 +1017,21 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
   double t_sync = 0.0;  // seconds spent waiting on the device inside the sweep loop
   int sweeps = 0;
   const Layout& L = c->lay;
-  const long long n = L.n;
+  // which >= 0: modality, -1: modality average, kOmnibus: the m n x m n
+  // imputed omnibus matrix
+  const long long n = (which == kOmnibus) ? static_cast<long long>(L.m) * L.n : L.n;
   if (d < 1 || static_cast<long long>(d) > n)
     return set_error(JOFC_EINVAL, "cmds: dimension out of range");
   DevBuf<double> S, aux;
   JOFC_CUDA(S.ensure(static_cast<size_t>(n) * n));
   JOFC_CUDA(aux.ensure(static_cast<size_t>(n) + 1));
   JOFC_CUDA(cudaMemsetAsync(S.p, 0, static_cast<size_t>(n) * n * sizeof(double), c->stream));
-  init::dense_d2_kernel<<<static_cast<unsigned>(L.bpm), 256, 0, c->stream>>>(
-      c->delta.p, n, L.nT, L.bpm, L.m, which, S.p);
+  if (which == kOmnibus)
+    init::omnibus_d2_kernel<<<static_cast<unsigned>(L.bpm), 256, 0, c->stream>>>(
+        c->delta.p, L.n, L.nT, L.bpm, L.m, S.p);
+  else
+    init::dense_d2_kernel<<<static_cast<unsigned>(L.bpm), 256, 0, c->stream>>>(
+        c->delta.p, n, L.nT, L.bpm, L.m, which, S.p);
   JOFC_CUDA(cudaGetLastError());
   init::row_sums_kernel<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, c->stream>>>(S.p, n,
                                                                                           aux.p);
@@ -1259,6 +1268,28 @@ int jofc_cmds(jofc_ctx* c, int modality, size_t d, double* x_out) {
   rc = cmds_gpu(c, modality, d, x);
   if (rc) return rc;
   JOFC_CUDA(cudaMemcpy(x_out, x.a.data(), x.a.size() * sizeof(double), cudaMemcpyDefault));
+  return JOFC_OK;
+}
+
+int jofc_init_imputed_cmds(jofc_ctx* c, size_t d, size_t dense_cap, double* x_out) {
+  int rc = require_full_problem(c);
+  if (rc) return rc;
+  const size_t m = static_cast<size_t>(c->lay.m), n = static_cast<size_t>(c->lay.n);
+  if (m * n > dense_cap)
+    return set_error(JOFC_EINVAL, "imputed_omnibus_init: mn exceeds the dense cap");
+  JOFC_CUDA(cudaSetDevice(c->device));
+  init::Mat x;
+  rc = cmds_gpu(c, kOmnibus, d, x);
+  if (rc) return rc;
+  // Configuration::from_stacked, then each block re-centred (init.cpp:111-114)
+  std::vector<double> out(m * n * d);
+  for (size_t l = 0; l < m; ++l) {
+    init::Mat blk(n, d);
+    std::copy(x.a.begin() + l * n * d, x.a.begin() + (l + 1) * n * d, blk.a.begin());
+    init::center_columns(blk);
+    std::copy(blk.a.begin(), blk.a.end(), out.begin() + l * n * d);
+  }
+  JOFC_CUDA(cudaMemcpy(x_out, out.data(), out.size() * sizeof(double), cudaMemcpyDefault));
   return JOFC_OK;
 }
 

@@ -64,6 +64,42 @@ __global__ void __launch_bounds__(256) dense_d2_kernel(const double* __restrict_
   }
 }
 
+// Dense squared omnibus dissimilarity (N = m n) of imputed_omnibus_init
+// (proj/src/init.cpp:90-116): block (bi, bj) holds Delta_bi for bi == bj and
+// 0.5 (Delta_bi + Delta_bj) otherwise (same rounding as the host), each entry
+// then squared as cmds does.  One CTA per packed block of modality 0's stream
+// coordinates; every unordered modality pair writes its four mirror entries.
+__global__ void __launch_bounds__(256) omnibus_d2_kernel(const double* __restrict__ packed,
+                                                         long long n, int nT, long long bpm, int m,
+                                                         double* __restrict__ d2) {
+  const long long g0 = blockIdx.x;
+  int l0, B, J;
+  block_coords(g0, nT, bpm, l0, B, J);
+  const long long N = static_cast<long long>(m) * n;
+  const long long gi0 = static_cast<long long>(kRows) * B, gj0 = static_cast<long long>(kCols) * J;
+  for (int e = threadIdx.x; e < kBlockElems; e += blockDim.x) {
+    const int jl = e >> 7, il = e & 127;
+    const long long i = gi0 + il, j = gj0 + jl;
+    if (!(i < j && j < n)) continue;
+    for (int bi = 0; bi < m; ++bi) {
+      const double a = packed[(static_cast<long long>(bi) * bpm + g0) * kBlockElems + e];
+      for (int bj = bi; bj < m; ++bj) {
+        double v = a;
+        if (bj != bi)
+          v = __dmul_rn(0.5, __dadd_rn(a, packed[(static_cast<long long>(bj) * bpm + g0) * kBlockElems + e]));
+        const double sq = __dmul_rn(v, v);
+        const long long ri = bi * n, rj = static_cast<long long>(bj) * n;
+        d2[(rj + j) * N + ri + i] = sq;
+        d2[(ri + i) * N + rj + j] = sq;
+        if (bj != bi) {
+          d2[(rj + i) * N + ri + j] = sq;
+          d2[(ri + j) * N + rj + i] = sq;
+        }
+      }
+    }
+  }
+}
+
 // Row sums of a dense n x n matrix: one warp per row.
 __global__ void __launch_bounds__(256) row_sums_kernel(const double* __restrict__ a, long long n,
                                                        double* __restrict__ out) {

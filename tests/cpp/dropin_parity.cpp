@@ -202,6 +202,15 @@ static void default_init_runs() {
   CHECK(r.iterations >= 1);
   for (std::size_t t = 1; t < r.stress_trace.size(); ++t)
     CHECK(r.stress_trace[t] <= r.stress_trace[t - 1] + 1e-9);
+  SolveOptions imp = opt;
+  imp.init = InitKind::imputed_cmds;
+  const EmbeddingResult ri = fjofc_embed(problem, WeightSpec::uniform(1.0), imp);
+  CHECK(ri.iterations >= 1);
+  const Configuration start = imputed_omnibus_init(problem, 2);
+  CHECK(std::abs(raw_stress(start, problem, WeightSpec::uniform(1.0)) - ri.stress_trace[0]) <=
+        1e-10 * ri.stress_trace[0]);
+  imp.dense_cap = 100;
+  CHECK(throws<std::invalid_argument>([&] { fjofc_embed(problem, WeightSpec::uniform(1.0), imp); }));
   const Configuration init = averaged_procrustes_init(problem, 2);
   CHECK(init.modality_count() == 2 && init.object_count() == 120 && init.dim() == 2);
   CHECK(std::abs(raw_stress(init, problem, WeightSpec::uniform(1.0)) - r.stress_trace[0]) <=
@@ -240,6 +249,7 @@ static void errors() {
   CHECK(throws<std::invalid_argument>(
       [&] { guttman_step_fast(wrong, problem, WeightSpec::uniform(1.0)); }));
   opt.init = InitKind::imputed_cmds;
+  opt.dense_cap = 1;  // m n above the cap: the reference's invalid_argument
   CHECK(throws<std::invalid_argument>([&] { fjofc_embed(problem, WeightSpec::uniform(1.0), opt); }));
   DenseMatrix asym = problem.modality(0);
   asym(0, 1) += 1.0;

@@ -81,3 +81,25 @@ def test_cmds_low_rank(R):
         ref = R.cmds(delta, modality, 3)
         got = jg.cmds(prob, modality, 3)
         assert rel_fro(got, ref) < 1e-7, (modality, rel_fro(got, ref))
+
+
+@pytest.mark.parametrize("n,m,d,tol", [(60, 3, 2, 1e-12), (150, 2, 3, 1e-12),
+                                       (400, 2, 2, 1e-7), (300, 3, 3, 1e-7)])
+def test_imputed_omnibus_init_matches_reference(R, n, m, d, tol):
+    delta = problem(n, m=m, seed=n + m)
+    prob = jg.OmnibusProblem(list(delta), validate=False)
+    ref = R.imputed_omnibus_init(delta, d)
+    got = jg.imputed_omnibus_init(prob, d)
+    assert rel_fro(got, ref) < tol, rel_fro(got, ref)
+
+
+def test_imputed_dense_cap(R):
+    delta = problem(100, m=2, seed=1)
+    prob = jg.OmnibusProblem(list(delta), validate=False)
+    with pytest.raises(jg.InvalidArgument, match="mn exceeds the dense cap"):
+        jg.imputed_omnibus_init(prob, 2, dense_cap=150)
+    opt = jg.SolveOptions(dim=2, eps=1e-300, max_iterations=20, init=jg.InitKind.imputed_cmds)
+    got = jg.fjofc_embed(prob, jg.WeightSpec.uniform(1.0), opt)
+    x0 = R.imputed_omnibus_init(delta, 2)
+    ref = R.fjofc_embed(delta, Spec.uniform(1.0), x0, 1e-300, 20)
+    assert rel_fro(got.config, ref.x) < 1e-8
