@@ -17,7 +17,8 @@ GPU_HDR := $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/jofc_gpu.h include/jofc
 DROPIN_SRC := $(wildcard $(CSRC)/dropin/*.cpp)
 DROPIN_HDR := $(wildcard include/jofc/*.hpp)
 
-all: $(PKG)/libjofc_gpu.so $(PKG)/libjofc.so $(PKG)/libjofc_probe.so oracle build/dropin_parity
+all: $(PKG)/libjofc_gpu.so $(PKG)/libjofc.so $(PKG)/libjofc_probe.so oracle build/dropin_parity \
+     build/jofc
 
 $(PKG)/libjofc_probe.so: $(CSRC)/probe.cu
 	$(NVCC) $(NVFLAGS) -shared -o $@ $<
@@ -38,6 +39,12 @@ build/dropin_parity: tests/cpp/dropin_parity.cpp $(PKG)/libjofc.so oracle/jofc_o
 	$(MAKE) -C oracle all
 	$(CXX) -std=c++20 -O2 -Iinclude -Ioracle -o $@ $< -L$(PKG) -ljofc -ljofc_gpu \
 	    -Loracle -ljofc_oracle -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,'$$ORIGIN/../oracle'
+
+# command-line front end (tools/jofc_cli.cpp) on the drop-in API + C ABI
+build/jofc: tools/jofc_cli.cpp $(PKG)/libjofc.so $(DROPIN_HDR) include/jofc_gpu.h
+	@mkdir -p build
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -ljofc -ljofc_gpu \
+	    -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 ref:
 	$(MAKE) -C oracle ref

@@ -314,6 +314,18 @@ class Reference:
         finally:
             L.ref_problem_destroy(h)
 
+    def simulate_save(self, setting, n, m, dim, n_anom, seed, out):
+        self.lib.ref_simulate_save.argtypes = [C.c_char_p, _sz, _sz, _sz, _sz, C.c_uint64,
+                                               C.c_char_p]
+        self._check(self.lib.ref_simulate_save(setting.encode(), n, m, dim, n_anom, seed,
+                                               os.fsencode(out)))
+
+    def parse_run_config(self, path):
+        """None when the reference accepts the file, else its message."""
+        self.lib.ref_parse_run_config.argtypes = [C.c_char_p]
+        rc = self.lib.ref_parse_run_config(os.fsencode(path))
+        return None if rc == 0 else self.lib.ref_last_error().decode()
+
     def save_problem_binary(self, delta, path):
         """proj/src/io.cpp:217-223 (the reference's own .jofc writer)."""
         self._check(self.lib.ref_save_problem_binary(self.problem(delta), os.fsencode(path)))

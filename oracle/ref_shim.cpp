@@ -19,6 +19,7 @@
 #include "jofc/distance.hpp"
 #include "jofc/init.hpp"
 #include "jofc/io.hpp"
+#include "jofc/simulate.hpp"
 #include "jofc/linalg.hpp"
 #include "jofc/oos.hpp"
 #include "jofc/problem.hpp"
@@ -180,6 +181,33 @@ void* ref_load_dissimilarities(const char* const* paths, size_t count) {
     out = new OmnibusProblem(load_dissimilarities(ps));
   });
   return rc ? nullptr : out;
+}
+
+// The reference library calls behind `jofc simulate` (the CLI's own file
+// naming, proj/tools/jofc_main.cpp:108-139, restated here for the test).
+int ref_simulate_save(const char* setting, size_t n, size_t m, size_t dim, size_t n_anom,
+                      uint64_t seed, const char* out_c) {
+  return guarded([&] {
+    const std::string out = out_c;
+    const SimulatedProblem sim = std::string(setting) == "matched"
+                                     ? generate_matched(n, m, dim, seed)
+                                     : generate_anomaly(n, m, n_anom, dim, seed);
+    const bool binary = out.size() > 5 && out.substr(out.size() - 5) == ".jofc";
+    if (binary) {
+      save_problem_binary(out, sim.problem());
+    } else {
+      for (size_t i = 0; i < sim.modalities.size(); ++i)
+        save_csv_matrix(out + "_" + std::to_string(i + 1) + ".csv", sim.modalities[i]);
+    }
+    save_labels(binary ? out + ".labels.csv" : out + "_labels.csv", sim.labels);
+    if (!sim.anomalies.empty())
+      save_indices(binary ? out + ".anomalies.csv" : out + "_anomalies.csv", sim.anomalies);
+  });
+}
+
+// parse_run_config (proj/src/io.cpp:354-460): 0, or 1 with the message.
+int ref_parse_run_config(const char* path) {
+  return guarded([&] { (void)parse_run_config(path); });
 }
 
 int ref_problem_shape(void* prob, size_t* m, size_t* n) {
