@@ -128,8 +128,8 @@ def h2d_bytes_dense_upload(m, n, world, rank):
     return b
 
 
-def read_traffic(cfg):
-    path = os.path.join(ROOT, "profiles", f"pass_traffic_cfg{cfg}.json")
+def read_traffic(cfg, kind="pass"):
+    path = os.path.join(ROOT, "profiles", f"{kind}_traffic_cfg{cfg}.json")
     if os.path.exists(path):
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_launch")
@@ -651,7 +651,8 @@ def run_init(args):
                    "l2": f"S is {s_bytes / 1e9:.2f} GB per solve, larger than L2"},
         "sweeps_per_s": round(sweeps * args.steps / sec, 1), "sweeps_per_init": sweeps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
-                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                     "traffic": read_traffic(wl.cfg, "init"),
                      "peak_source": hbm_src, "kernel": "matvec_sym_kernel (S Q)",
                      "kernel_ms": round(mv_avg_ms, 4),
                      "share_of_step": round(mv_share, 4)},
