@@ -26,6 +26,11 @@ $(PKG)/libjofc_probe.so: $(CSRC)/probe.cu
 $(PKG)/libjofc_gpu.so: $(GPU_SRC) $(GPU_HDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPU_SRC) -lgomp
 
+# kernel experiments: `make exp EXP=-DJOFC_EXP_...` builds the same C ABI with an
+# experimental switch into libjofc_gpu_exp.so (selected with JOFC_GPU_LIB)
+exp:
+	$(NVCC) $(NVFLAGS) $(EXP) -shared -o $(PKG)/libjofc_gpu_exp.so $(GPU_SRC) -lgomp
+
 $(PKG)/libjofc.so: $(DROPIN_SRC) $(DROPIN_HDR) $(PKG)/libjofc_gpu.so
 	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(DROPIN_SRC) \
 	    -L$(PKG) -ljofc_gpu -Wl,-rpath,'$$ORIGIN'
@@ -56,4 +61,4 @@ clean:
 	rm -f $(PKG)/*.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle ref sass clean
+.PHONY: all oracle ref sass clean exp

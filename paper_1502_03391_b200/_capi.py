@@ -106,10 +106,13 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing; build it with `make` "
+    # JOFC_GPU_LIB: an alternative in-tree build of the same C ABI (kernel
+    # experiments, scripts/diag_pass.py); the default is the shipped library
+    path = os.environ.get("JOFC_GPU_LIB", LIB_PATH)
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing; build it with `make` "
                           "(or __graft_entry__.build()).  There is no CPU fallback.")
-    lib = C.CDLL(LIB_PATH)
+    lib = C.CDLL(path)
     for name, (res, args) in _SIGS.items():
         fn = getattr(lib, name)
         fn.restype = res
