@@ -57,6 +57,12 @@ int set_error(int code, const char* fmt, ...) {
                        __FILE__, __LINE__);                                             \
   } while (0)
 
+#define JOFC_TRY(call)     \
+  do {                     \
+    const int rc_ = (call); \
+    if (rc_) return rc_;   \
+  } while (0)
+
 constexpr int kMaxD = 10;
 
 template <class T>
@@ -153,6 +159,9 @@ struct jofc_ctx {
   DevBuf<OosPoint> oos_st;
   // streaming ingest staging
   IngestPanels ingest;
+  // host -> device upload: copies on their own stream, overlapped with packing
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t up_copied[2] = {nullptr, nullptr}, up_packed[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -211,6 +220,15 @@ int launch_epi(jofc_ctx* c, const EpiParams& ep) {
     default:                                \
       return set_error(JOFC_EINVAL, "dim %zu unsupported (1..10)", static_cast<size_t>(d)); \
   }
+
+// Synchronous copy ordered on the context stream (the context stream is a
+// non-blocking stream: a plain cudaMemcpy on the legacy stream would not wait
+// for its kernels, and a pageable H2D cudaMemcpy may return before the DMA).
+int copy_sync(jofc_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  JOFC_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  return JOFC_OK;
+}
 
 // When profiling, records the start event of the next profiled launch on the
 // context stream and hands back its end event (else leaves *end null).
@@ -512,6 +530,11 @@ int jofc_ctx_destroy(jofc_ctx* c) {
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   if (c->ctrl_host) cudaFreeHost(c->ctrl_host);
   c->ingest.release();
+  for (int k = 0; k < 2; ++k) {
+    if (c->up_copied[k]) cudaEventDestroy(c->up_copied[k]);
+    if (c->up_packed[k]) cudaEventDestroy(c->up_packed[k]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return JOFC_OK;
@@ -606,30 +629,47 @@ int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta
     }
 
   // Staging: up to kChunk row blocks (128 rows each) of the dense matrix,
-  // columns from the chunk's first row onwards (the upper part only).
+  // columns from the chunk's first row onwards (the upper part only).  Two
+  // stage buffers: the copy of chunk k+1 (copy stream) runs under the packing
+  // of chunk k (context stream).
   const int kChunk = 4;
-  DevBuf<double> stage;
+  if (!c->copy_stream) {
+    JOFC_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      JOFC_CUDA(cudaEventCreateWithFlags(&c->up_copied[k], cudaEventDisableTiming));
+      JOFC_CUDA(cudaEventCreateWithFlags(&c->up_packed[k], cudaEventDisableTiming));
+    }
+  }
+  DevBuf<double> stage[2];
   DevBuf<int> bad;
-  JOFC_CUDA(stage.ensure(static_cast<size_t>(kChunk) * kRows * L.n_pad));
+  for (int k = 0; k < 2; ++k) JOFC_CUDA(stage[k].ensure(static_cast<size_t>(kChunk) * kRows * L.n_pad));
   JOFC_CUDA(bad.ensure(1));
   JOFC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+  // the copy stream starts after everything already queued on the context stream
+  JOFC_CUDA(cudaEventRecord(c->up_packed[0], c->stream));
+  JOFC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->up_packed[0], 0));
+  long long chunk = 0;
   for (int l = 0; l < L.m; ++l) {
     for (int B0 = 0; B0 < L.nB; B0 += kChunk) {
       const int B1 = std::min(L.nB, B0 + kChunk);
       const long long g_lo = static_cast<long long>(l) * L.bpm + row_first(L.nT, B0);
       const long long g_hi = static_cast<long long>(l) * L.bpm + row_first(L.nT, B1);
       if (g_hi <= L.begin || g_lo >= L.end) continue;  // not in this shard
+      const int k = static_cast<int>(chunk & 1);
       const long long r0 = static_cast<long long>(B0) * kRows;
       const long long r1 = std::min<long long>(L.n, static_cast<long long>(B1) * kRows);
       const long long c0 = r0;
+      if (chunk >= 2) JOFC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->up_packed[k], 0));
       if (r1 > r0 && c0 < L.n) {
         const size_t width = static_cast<size_t>(L.n - c0) * sizeof(double);
-        JOFC_CUDA(cudaMemcpy2DAsync(stage.p, L.n_pad * sizeof(double), delta[l] + r0 * L.n + c0,
+        JOFC_CUDA(cudaMemcpy2DAsync(stage[k].p, L.n_pad * sizeof(double), delta[l] + r0 * L.n + c0,
                                     L.n * sizeof(double), width, static_cast<size_t>(r1 - r0),
-                                    cudaMemcpyDefault, c->stream));
+                                    cudaMemcpyDefault, c->copy_stream));
       }
+      JOFC_CUDA(cudaEventRecord(c->up_copied[k], c->copy_stream));
+      JOFC_CUDA(cudaStreamWaitEvent(c->stream, c->up_copied[k], 0));
       PackParams pk{};
-      pk.stage = stage.p;
+      pk.stage = stage[k].p;
       pk.pitch = L.n_pad;
       pk.r0 = r0;
       pk.c0 = c0;
@@ -644,14 +684,14 @@ int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta
       pk.bad = bad.p;
       jofc_pack_kernel<<<static_cast<unsigned>(g_hi - g_lo), 256, 0, c->stream>>>(pk);
       JOFC_CUDA(cudaGetLastError());
+      JOFC_CUDA(cudaEventRecord(c->up_packed[k], c->stream));
       ++c->launches;
+      ++chunk;
     }
   }
   int hbad = 0;
   JOFC_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
-  stage.release();
-  bad.release();
   if (hbad) return set_error(JOFC_EINVAL, "OmnibusProblem: delta has a non-finite or negative entry");
   c->has_problem = true;
   return JOFC_OK;
@@ -925,7 +965,7 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
     }
   }
   if (y_out)  // y_out may be host or device memory
-    JOFC_CUDA(cudaMemcpy(y_out, y_all.data(), y_all.size() * sizeof(double), cudaMemcpyDefault));
+    JOFC_TRY(copy_sync(c, y_out, y_all.data(), y_all.size() * sizeof(double), cudaMemcpyDefault));
   return JOFC_OK;
 }
 
@@ -1067,7 +1107,7 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
   if (n <= 320 || k + 4 >= static_cast<size_t>(n)) {
     // the reference's dense route (cyclic Jacobi on the whole S)
     init::Mat h(n, n);
-    JOFC_CUDA(cudaMemcpy(h.a.data(), S.p, h.a.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    JOFC_TRY(copy_sync(c, h.a.data(), S.p, h.a.size() * sizeof(double), cudaMemcpyDeviceToHost));
     std::vector<double> ev;
     init::Mat v;
     if (!init::jacobi_eigen(h, ev, v))
@@ -1190,7 +1230,7 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
         if (std::sqrt(acc[cc]) > tol) conv = false;
       if (conv) {
         init::Mat ritz(n, k);
-        JOFC_CUDA(cudaMemcpy(ritz.a.data(), dritz.p, ritz.a.size() * sizeof(double),
+        JOFC_TRY(copy_sync(c, ritz.a.data(), dritz.p, ritz.a.size() * sizeof(double),
                              cudaMemcpyDeviceToHost));
         for (size_t cc = 0; cc < k; ++cc) {
           std::vector<double> col(n);
@@ -1208,10 +1248,10 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
         break;
       }
       if (!chol) {  // ill-conditioned panel: the reference's Gram-Schmidt on the host
-        JOFC_CUDA(cudaMemcpy(q.a.data(), dw.p, q.a.size() * sizeof(double),
+        JOFC_TRY(copy_sync(c, q.a.data(), dw.p, q.a.size() * sizeof(double),
                              cudaMemcpyDeviceToHost));
         init::orthonormalize(q);
-        JOFC_CUDA(cudaMemcpy(dq.p, q.a.data(), q.a.size() * sizeof(double),
+        JOFC_TRY(copy_sync(c, dq.p, q.a.data(), q.a.size() * sizeof(double),
                              cudaMemcpyHostToDevice));
         continue;
       }
@@ -1224,10 +1264,10 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
         ++c->launches;
         JOFC_CUDA(cudaGetLastError());
       } else {
-        JOFC_CUDA(cudaMemcpy(q.a.data(), dq.p, q.a.size() * sizeof(double),
+        JOFC_TRY(copy_sync(c, q.a.data(), dq.p, q.a.size() * sizeof(double),
                              cudaMemcpyDeviceToHost));
         init::orthonormalize(q);
-        JOFC_CUDA(cudaMemcpy(dq.p, q.a.data(), q.a.size() * sizeof(double),
+        JOFC_TRY(copy_sync(c, dq.p, q.a.data(), q.a.size() * sizeof(double),
                              cudaMemcpyHostToDevice));
       }
     }
@@ -1267,7 +1307,7 @@ int jofc_cmds(jofc_ctx* c, int modality, size_t d, double* x_out) {
   init::Mat x;
   rc = cmds_gpu(c, modality, d, x);
   if (rc) return rc;
-  JOFC_CUDA(cudaMemcpy(x_out, x.a.data(), x.a.size() * sizeof(double), cudaMemcpyDefault));
+  JOFC_TRY(copy_sync(c, x_out, x.a.data(), x.a.size() * sizeof(double), cudaMemcpyDefault));
   return JOFC_OK;
 }
 
@@ -1289,7 +1329,7 @@ int jofc_init_imputed_cmds(jofc_ctx* c, size_t d, size_t dense_cap, double* x_ou
     init::center_columns(blk);
     std::copy(blk.a.begin(), blk.a.end(), out.begin() + l * n * d);
   }
-  JOFC_CUDA(cudaMemcpy(x_out, out.data(), out.size() * sizeof(double), cudaMemcpyDefault));
+  JOFC_TRY(copy_sync(c, x_out, out.data(), out.size() * sizeof(double), cudaMemcpyDefault));
   return JOFC_OK;
 }
 
@@ -1311,7 +1351,7 @@ int jofc_init_averaged_procrustes(jofc_ctx* c, size_t d, double* x_out) {
     const init::Mat rot = init::procrustes(xl, anchor);
     std::copy(rot.a.begin(), rot.a.end(), out.begin() + l * block);
   }
-  JOFC_CUDA(cudaMemcpy(x_out, out.data(), out.size() * sizeof(double), cudaMemcpyDefault));
+  JOFC_TRY(copy_sync(c, x_out, out.data(), out.size() * sizeof(double), cudaMemcpyDefault));
   return JOFC_OK;
 }
 
@@ -1594,7 +1634,7 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
     for (long long l = 0; l < m; ++l) {
       jofc_sumsq_kernel<<<grid, 256, 0, c->stream>>>(c->delta.p, l * L.bpm, L.bpm, part.p);
       JOFC_CUDA(cudaGetLastError());
-      JOFC_CUDA(cudaMemcpy(hp.data(), part.p, grid * sizeof(double), cudaMemcpyDeviceToHost));
+      JOFC_TRY(copy_sync(c, hp.data(), part.p, grid * sizeof(double), cudaMemcpyDeviceToHost));
       double s = 0.0;
       for (double v : hp) s += v;
       const double norm = std::sqrt(2.0 * s);
