@@ -325,7 +325,9 @@ class Device:
         feats = _f64(feats)
         m, n, p = feats.shape
         check(self.lib.jofc_set_problem_features(self.h, m, n, p, dptr(feats)))
-        self._problem_key = ("features", id(feats))
+        self._problem_key = ("features", id(feats), object())
+        self._keep = None
+        return ResidentProblem(self, m, n, self._problem_key)
 
     def problem_bytes(self):
         return int(self.lib.jofc_problem_bytes(self.h))

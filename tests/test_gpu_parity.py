@@ -233,6 +233,27 @@ def test_config3_reduced(dev, P):
     _config_parity(dev, P, 3, n=2500, iters=20)
 
 
+# Full BASELINE sizes and iteration counts (C3: 2 x 20000^2, C4: 10 x 10000^2
+# dense host Delta, 100 iterations) against the reference library itself
+# (oracle/_ref, OpenMP on the host cores): every stress-trace entry, the
+# iteration count and the final X.  Then the bench's path (Delta built on the
+# device from the features, bit-identical) reproduces that solve.
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_against_reference(dev, P, cfg):
+    r = _config_parity(dev, P, cfg)
+    wl = workloads.make(cfg)
+    assert r.iterations == wl.iterations
+    tr = r.stress_trace
+    assert all(b < a for a, b in zip(tr, tr[1:]))  # strict decrease: the stop rule never fired
+    opt = jg.SolveOptions(dim=wl.d, eps=1e-300, max_iterations=wl.iterations,
+                          init=jg.InitKind.provided, init_config=wl.x0())
+    prob = dev.upload_features(wl.in_features)
+    again = jg.fjofc_embed(prob, wl.spec, opt, device=dev)
+    assert again.iterations == r.iterations
+    assert max(rel(a, b) for a, b in zip(again.stress_trace, tr)) < 1e-12
+    assert rel_fro(again.config, r.config) < 1e-12
+
+
 # ------------------------------------------------------------------ out-of-sample
 def test_oos_golden(dev, golden):
     for i in range(int(golden["n_oos"])):
