@@ -47,6 +47,10 @@ struct OosParams {
 constexpr int kOosWarps = 8;
 constexpr int kOosChunk = 512;
 constexpr int kOosSplits = 4;  // n-range slices per (point, modality): 4x the warps in flight
+#ifndef JOFC_OOS_UNROLL
+#define JOFC_OOS_UNROLL 4
+#endif
+constexpr int kOosUnroll = JOFC_OOS_UNROLL;  // delta entries per lane per step
 
 template <int D>
 __global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_pass_kernel(const OosParams p) {
@@ -69,48 +73,63 @@ __global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_pass_kernel(const Oos
   for (int c = 0; c < D; ++c) y[c] = active ? yb[c] : 0.0;
   const double* X = p.x + static_cast<long long>(j) * p.n * D;
   const double* dl = p.deltas + (static_cast<long long>(pt) * p.m + j) * p.n;
-  double psi = 0.0, fid = 0.0, xi[D];
+  double psi[2] = {0.0, 0.0}, fid[2] = {0.0, 0.0}, xi[2][D];
 #pragma unroll
-  for (int c = 0; c < D; ++c) xi[c] = 0.0;
+  for (int c = 0; c < D; ++c) xi[0][c] = xi[1][c] = 0.0;
   for (long long k0 = k_lo; k0 < k_hi; k0 += kOosChunk) {
     const int rows = static_cast<int>(min(static_cast<long long>(kOosChunk), k_hi - k0));
     __syncthreads();
     for (int e = threadIdx.x; e < rows * D; e += blockDim.x) xs[e] = X[k0 * D + e];
     __syncthreads();
     if (!active) continue;
-    for (int kk = lane; kk < rows; kk += 32) {
-      const double dv = dl[k0 + kk];
-      double s = 0.0, xk[D];
+    // kOosUnroll delta loads in flight per lane, two accumulator sets
+    for (int kk0 = lane; kk0 < rows; kk0 += 32 * kOosUnroll) {
+      double dv[kOosUnroll];
 #pragma unroll
-      for (int c = 0; c < D; ++c) {
-        xk[c] = xs[kk * D + c];
-        const double df = xk[c] - y[c];
-        s = (c == 0) ? df * df : fma(df, df, s);
+      for (int u = 0; u < kOosUnroll; ++u) {
+        const int kk = kk0 + 32 * u;
+        dv[u] = (kk < rows) ? dl[k0 + kk] : 0.0;
       }
-      const double inv = (s > 0.0) ? rsqrt_nr(s) : 0.0;
-      const double r = dv * inv;
-      const double resid = dv - s * inv;
-      fid = fma(resid, resid, fid);
-      psi += r;
-      const double cf = 1.0 - r;
 #pragma unroll
-      for (int c = 0; c < D; ++c) xi[c] = fma(cf, xk[c], xi[c]);
+      for (int u = 0; u < kOosUnroll; ++u) {
+        const int kk = kk0 + 32 * u;
+        if (kk >= rows) break;
+        double s = 0.0, xk[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          xk[c] = xs[kk * D + c];
+          const double df = xk[c] - y[c];
+          s = (c == 0) ? df * df : fma(df, df, s);
+        }
+        const double inv = (s > 0.0) ? rsqrt_nr(s) : 0.0;
+        const double r = dv[u] * inv;
+        const double resid = dv[u] - s * inv;
+        const int a = u & 1;
+        fid[a] = fma(resid, resid, fid[a]);
+        psi[a] += r;
+        const double cf = 1.0 - r;
+#pragma unroll
+        for (int c = 0; c < D; ++c) xi[a][c] = fma(cf, xk[c], xi[a][c]);
+      }
     }
   }
   if (!active) return;
+  double spsi = psi[0] + psi[1], sfid = fid[0] + fid[1], sxi[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) sxi[c] = xi[0][c] + xi[1][c];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    psi += __shfl_xor_sync(0xffffffffu, psi, o);
-    fid += __shfl_xor_sync(0xffffffffu, fid, o);
+    spsi += __shfl_xor_sync(0xffffffffu, spsi, o);
+    sfid += __shfl_xor_sync(0xffffffffu, sfid, o);
 #pragma unroll
-    for (int c = 0; c < D; ++c) xi[c] += __shfl_xor_sync(0xffffffffu, xi[c], o);
+    for (int c = 0; c < D; ++c) sxi[c] += __shfl_xor_sync(0xffffffffu, sxi[c], o);
   }
   if (lane == 0) {  // slices of the n range meet in `part` (zeroed by the update kernel)
     double* out = p.part + (static_cast<long long>(pt) * p.m + j) * (D + 2);
-    atomicAdd(out, psi);
-    atomicAdd(out + 1, fid);
+    atomicAdd(out, spsi);
+    atomicAdd(out + 1, sfid);
 #pragma unroll
-    for (int c = 0; c < D; ++c) atomicAdd(out + 2 + c, xi[c]);
+    for (int c = 0; c < D; ++c) atomicAdd(out + 2 + c, sxi[c]);
   }
 }
 
