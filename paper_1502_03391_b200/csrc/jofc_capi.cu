@@ -857,8 +857,12 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
       c->graphs.clear();
     }
     JOFC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    constexpr int smem = oos_smem_bytes<D>();
+    if (smem > 48 * 1024)
+      JOFC_CUDA(cudaFuncSetAttribute(jofc_oos_pass_kernel<D>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     for (int t = 0; t <= steps; ++t) {
-      jofc_oos_pass_kernel<D><<<pg, kOosWarps * 32, 0, c->stream>>>(op);
+      jofc_oos_pass_kernel<D><<<pg, kOosWarps * 32, smem, c->stream>>>(op);
       jofc_oos_update_kernel<D><<<ug, 128, 0, c->stream>>>(op);
     }
     cudaGraph_t g = nullptr;
@@ -887,7 +891,7 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
   if (d < 1 || d > static_cast<size_t>(kMaxD))
     return set_error(JOFC_EINVAL, "dim %zu unsupported (1..%d)", d, kMaxD);
   JOFC_CUDA(cudaSetDevice(c->device));
-  JOFC_CUDA(c->oos_x.ensure(m * n * d));
+  JOFC_CUDA(c->oos_x.ensure(m * n * d + 4));  // + slack: chunk copies round up to 16 bytes
   JOFC_CUDA(c->oos_delta.ensure(k * m * n));
   JOFC_CUDA(c->oos_y0.ensure(k * m * d));
   JOFC_CUDA(c->oos_y1.ensure(k * m * d));

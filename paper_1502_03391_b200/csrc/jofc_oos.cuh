@@ -12,10 +12,11 @@
 // term and the per-point stop rule (proj/src/oos.cpp:221-226).
 //
 // Pass layout: CTA = 8 warps = 8 points of one modality (blockIdx.y) and one
-// of kOosSplits slices of the in-sample range (blockIdx.z); X^(j)
-// is staged through shared memory in 512-row chunks and shared by the 8
-// warps; lanes stride the n in-sample rows (coalesced delta reads), warp
-// shuffles finish the sums.
+// of kOosSplits slices of the in-sample range (blockIdx.z); X^(j) streams
+// through two shared-memory chunk buffers (512 rows each, filled by the TMA
+// bulk engine, double buffered) shared by the 8 warps; lanes stride the n
+// in-sample rows (coalesced delta reads, 4 in flight per lane), warp shuffles
+// finish the sums.
 #pragma once
 
 #include "jofc_kernels.cuh"
@@ -52,14 +53,25 @@ constexpr int kOosSplits = 4;  // n-range slices per (point, modality): 4x the w
 #endif
 constexpr int kOosUnroll = JOFC_OOS_UNROLL;  // delta entries per lane per step
 
+// X staging: two chunk buffers filled by the TMA bulk engine (double
+// buffered: chunk c + 2 streams in while chunk c + 1 is consumed).  Each buffer
+// has 2 spare doubles: a chunk's global start is rounded down to 16 bytes.
+template <int D>
+__host__ __device__ constexpr int oos_buf_doubles() { return kOosChunk * D + 2; }
+template <int D>
+__host__ __device__ constexpr int oos_smem_bytes() { return 128 + 2 * oos_buf_doubles<D>() * 8; }
+
 template <int D>
 __global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_pass_kernel(const OosParams p) {
-  __shared__ double xs[kOosChunk * D];
+  extern __shared__ __align__(128) unsigned char oos_smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(oos_smem);
+  double* xbuf = reinterpret_cast<double*>(oos_smem + 128);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pt = blockIdx.x * kOosWarps + warp;
   const int j = blockIdx.y;
   const long long k_lo = p.n * blockIdx.z / gridDim.z;
   const long long k_hi = p.n * (blockIdx.z + 1) / gridDim.z;
+  const int nch = static_cast<int>((k_hi - k_lo + kOosChunk - 1) / kOosChunk);
   bool active = pt < p.k;
   int t = 0;
   if (active) {
@@ -71,46 +83,69 @@ __global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_pass_kernel(const Oos
   const double* yb = ((t & 1) ? p.y1 : p.y0) + (static_cast<long long>(pt) * p.m + j) * D;
 #pragma unroll
   for (int c = 0; c < D; ++c) y[c] = active ? yb[c] : 0.0;
-  const double* X = p.x + static_cast<long long>(j) * p.n * D;
+  const long long xbase = static_cast<long long>(j) * p.n * D;  // X^(j) in doubles
   const double* dl = p.deltas + (static_cast<long long>(pt) * p.m + j) * p.n;
+  auto issue = [&](int ch) {  // thread 0: chunk ch -> buffer ch & 1
+    const long long k0 = k_lo + static_cast<long long>(ch) * kOosChunk;
+    const int rows = static_cast<int>(min(static_cast<long long>(kOosChunk), k_hi - k0));
+    const long long first = xbase + k0 * D;
+    const long long start = first & ~1LL;  // 16-byte aligned
+    const uint32_t bytes = static_cast<uint32_t>(((first - start + rows * D) * 8 + 15) & ~15LL);
+    mbar_expect_tx(&bar[ch & 1], bytes);
+    bulk_g2s(xbuf + (ch & 1) * oos_buf_doubles<D>(), p.x + start, bytes, &bar[ch & 1]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+    if (nch > 0) issue(0);
+    if (nch > 1) issue(1);
+  }
+  __syncthreads();
   double psi[2] = {0.0, 0.0}, fid[2] = {0.0, 0.0}, xi[2][D];
 #pragma unroll
   for (int c = 0; c < D; ++c) xi[0][c] = xi[1][c] = 0.0;
-  for (long long k0 = k_lo; k0 < k_hi; k0 += kOosChunk) {
+  for (int ch = 0; ch < nch; ++ch) {
+    const long long k0 = k_lo + static_cast<long long>(ch) * kOosChunk;
     const int rows = static_cast<int>(min(static_cast<long long>(kOosChunk), k_hi - k0));
-    __syncthreads();
-    for (int e = threadIdx.x; e < rows * D; e += blockDim.x) xs[e] = X[k0 * D + e];
-    __syncthreads();
-    if (!active) continue;
-    // kOosUnroll delta loads in flight per lane, two accumulator sets
-    for (int kk0 = lane; kk0 < rows; kk0 += 32 * kOosUnroll) {
-      double dv[kOosUnroll];
+    mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
+    const double* xs = xbuf + (ch & 1) * oos_buf_doubles<D>() + ((xbase + k0 * D) & 1);
+    if (active) {
+      // kOosUnroll delta loads in flight per lane, two accumulator sets
+      for (int kk0 = lane; kk0 < rows; kk0 += 32 * kOosUnroll) {
+        double dv[kOosUnroll];
 #pragma unroll
-      for (int u = 0; u < kOosUnroll; ++u) {
-        const int kk = kk0 + 32 * u;
-        dv[u] = (kk < rows) ? dl[k0 + kk] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kOosUnroll; ++u) {
-        const int kk = kk0 + 32 * u;
-        if (kk >= rows) break;
-        double s = 0.0, xk[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-          xk[c] = xs[kk * D + c];
-          const double df = xk[c] - y[c];
-          s = (c == 0) ? df * df : fma(df, df, s);
+        for (int u = 0; u < kOosUnroll; ++u) {
+          const int kk = kk0 + 32 * u;
+          dv[u] = (kk < rows) ? dl[k0 + kk] : 0.0;
         }
-        const double inv = (s > 0.0) ? rsqrt_nr(s) : 0.0;
-        const double r = dv[u] * inv;
-        const double resid = dv[u] - s * inv;
-        const int a = u & 1;
-        fid[a] = fma(resid, resid, fid[a]);
-        psi[a] += r;
-        const double cf = 1.0 - r;
 #pragma unroll
-        for (int c = 0; c < D; ++c) xi[a][c] = fma(cf, xk[c], xi[a][c]);
+        for (int u = 0; u < kOosUnroll; ++u) {
+          const int kk = kk0 + 32 * u;
+          if (kk >= rows) break;
+          double s = 0.0, xk[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            xk[c] = xs[kk * D + c];
+            const double df = xk[c] - y[c];
+            s = (c == 0) ? df * df : fma(df, df, s);
+          }
+          const double inv = (s > 0.0) ? rsqrt_nr(s) : 0.0;
+          const double r = dv[u] * inv;
+          const double resid = dv[u] - s * inv;
+          const int a = u & 1;
+          fid[a] = fma(resid, resid, fid[a]);
+          psi[a] += r;
+          const double cf = 1.0 - r;
+#pragma unroll
+          for (int c = 0; c < D; ++c) xi[a][c] = fma(cf, xk[c], xi[a][c]);
+        }
       }
+    }
+    __syncthreads();  // every warp is done with this buffer
+    if (threadIdx.x == 0 && ch + 2 < nch) {
+      fence_proxy_async_smem();
+      issue(ch + 2);
     }
   }
   if (!active) return;

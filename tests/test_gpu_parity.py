@@ -266,6 +266,25 @@ def test_oos_golden(dev, golden):
         assert rel_fro(e.y, golden[p + "embed_y"]) < 1e-7, p
 
 
+@pytest.mark.parametrize("n,d", [(333, 10), (1031, 7), (517, 1), (2049, 3)])
+def test_oos_batch_odd_sizes_and_dims(dev, P, n, d):
+    # odd n and odd d: X chunks start off 16-byte boundaries (TMA staging), the
+    # widest d uses the > 48 KB shared-memory launch
+    rng = np.random.default_rng(n + d)
+    m, k = 2, 21
+    x = rng.normal(size=(m, n, d))
+    yt = rng.normal(size=(k, m, d))
+    od = np.stack([[np.sqrt(((x[l] - yt[q, l]) ** 2).sum(1)) + 0.05 * rng.random(n)
+                    for l in range(m)] for q in range(k)])
+    y0 = np.stack([jg.oos_start(x, 77 + q) for q in range(k)])
+    y, tr, its = jg.oos_embed_batch(x, od, 0.7, y0, jg.OosOptions(1e-300, 40),
+                                    fixed_iterations=True, device=dev)
+    yr, trr, itr = P.oos_batch(x, od, 0.7, y0, 1e-300, 40, fixed=True)
+    for q in range(k):
+        assert rel_fro(y[q], yr[q]) < X_TOL
+        assert np.max(np.abs(tr[q] - trr[q]) / np.abs(trr[q])) < S_TOL
+
+
 def test_oos_batch_config5(dev, P):
     wl = workloads.make(5, n=1200)
     x = P.fjofc_embed(wl.dense_delta(), Spec.uniform(wl.w), wl.x0(), 1e-300, 30).x
