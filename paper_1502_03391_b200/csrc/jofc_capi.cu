@@ -786,14 +786,9 @@ int jofc_raw_stress(jofc_ctx* c, const jofc_weights* spec, size_t d, const doubl
   JOFC_CUDA(cudaSetDevice(c->device));
   int rc = enqueue_solve(c, spec, d, x, 1.0, 0, nullptr);
   if (rc) return rc;
-  Control h;
-  JOFC_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl.p, sizeof(Control), cudaMemcpyDeviceToHost,
-                            c->stream));
   double s = 0.0;
   JOFC_CUDA(cudaMemcpyAsync(&s, c->trace.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
-  h = *c->ctrl_host;
-  (void)h;
   *stress = s;  // non-finite stress is returned as is (raw_stress does not throw)
   return JOFC_OK;
 }
