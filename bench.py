@@ -39,6 +39,25 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def rank_device(local, torch):
+    """The GPU of this rank: LOCAL_RANK (one process per GPU).  Test hook:
+    JOFC_BENCH_SHARE_GPU=1 maps ranks onto the visible GPUs round-robin so the
+    torchrun path runs on a 1-GPU box -- only with JOFC_DIST_BACKEND=gloo, whose
+    all-reduce is host-staged (no kernel ever waits on another rank's)."""
+    if os.environ.get("JOFC_BENCH_SHARE_GPU") == "1":
+        return local % max(1, torch.cuda.device_count())
+    return local
+
+
+def init_dist(local, torch, dist):
+    backend = os.environ.get("JOFC_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    return backend
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -146,9 +165,9 @@ def run_ours(args):
     from paper_1502_03391_b200._capi import check, dptr
 
     rank, world, local = env_rank()
+    local = rank_device(local, torch)
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    backend = init_dist(local, torch, dist) if world > 1 else None
     cfg = args.config
     wl = workloads.make(cfg)
     spec = wl.spec
@@ -204,7 +223,10 @@ def run_ours(args):
     e1.record(stream)
     e1.synchronize()
     launches = dev.launches() - launches0
-    its = fetch()
+    x_dev = np.empty_like(x0_host)
+    its_c, conv_c = C.c_size_t(), C.c_int()
+    check(lib.jofc_fetch_result(dev.h, dptr(x_dev), None, C.byref(its_c), C.byref(conv_c)))
+    its = its_c.value
     pass_ms, pass_n = C.c_double(), C.c_uint64()
     if not profile_live:
         check(lib.jofc_profile(dev.h, 1))
@@ -256,7 +278,7 @@ def run_ours(args):
     # ---------------- e2e through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, wl, dev, spec, world, rank, torch, dist)
+        e2e = run_e2e(args, wl, dev, spec, world, rank, torch, dist, x_dev)
 
     # ---------------- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -277,6 +299,8 @@ def run_ours(args):
                        "launch": "CUDA graph replay" if args.graphs else "stream launches",
                        "delta_bytes_resident_per_gpu": local_bytes,
                        "parallelism": f"delta-shard{world}" if world > 1 else "single",
+                       "collective": (f"{backend} all-reduce of P + fidelity per iteration"
+                                      if world > 1 else None),
                        "l2": "inputs larger than L2 (packed Delta %.2f GB vs 126 MB L2)" % (local_bytes / 1e9)
                        if local_bytes > 126e6 * 4 else "Delta may be L2-resident"},
             "delta_entries_per_s": value * pairs,
@@ -295,7 +319,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, wl, dev, spec, world, rank, torch, dist):
+def run_e2e(args, wl, dev, spec, world, rank, torch, dist, x_dev):
     """Same metric through the reference-facing C ABI with host buffers."""
     import ctypes as C
 
@@ -352,7 +376,8 @@ def run_e2e(args, wl, dev, spec, world, rank, torch, dist):
             "ms_per_step": round(sec / steps * 1e3, 2),
             "path": "jofc_set_problem(pinned dense host Delta) + jofc_fjofc_embed(host X0 -> "
                     "host X, trace); wall clock, synchronous C-ABI calls",
-            "x_final_matches_device_run": bool(np.all(np.isfinite(x_out)))}
+            "x_final_rel_diff_vs_device_run": float(np.linalg.norm(x_out - x_dev)
+                                                    / max(np.linalg.norm(x_dev), 1e-300))}
 
 
 def cpu_baseline(wl, args):
