@@ -164,6 +164,16 @@ int jofc_init_averaged_procrustes(jofc_ctx* ctx, size_t d, double* x_out);
  * modality blocks, each re-centred.  Rejects m n > dense_cap like the
  * reference. */
 int jofc_init_imputed_cmds(jofc_ctx* ctx, size_t d, size_t dense_cap, double* x_out);
+/* symmetric_top_eigenpairs_subspace (proj/include/jofc/linalg.hpp:29-35,
+ * proj/src/linalg.cpp:198-271): top-k eigenpairs by algebraic value of the
+ * symmetric n x n matrix s (row-major, host or device memory; symmetry is the
+ * caller's contract), descending.  n <= 64 or k + 4 >= n: the reference's
+ * cyclic Jacobi; else its shifted orthogonal iteration with the S Q products on
+ * the device.  values: k; vectors: k x n (eigenvector c at vectors + c n, unit
+ * norm, largest-magnitude component positive).  k + 4 <= 14 on the subspace
+ * route. */
+int jofc_symmetric_top_eigenpairs_subspace(jofc_ctx* ctx, size_t n, const double* s, size_t k,
+                                           double* values, double* vectors);
 
 #ifdef __cplusplus
 }

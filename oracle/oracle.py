@@ -314,6 +314,14 @@ class Reference:
         finally:
             L.ref_problem_destroy(h)
 
+    def symmetric_top_eigenpairs_subspace(self, s, k):
+        s = _f64(s)
+        n = s.shape[0]
+        vals, vecs = np.empty(k), np.empty((k, n))
+        self._check(self.lib.ref_symmetric_top_eigenpairs_subspace(_sz(n), _ptr(s), _sz(k),
+                                                                   _ptr(vals), _ptr(vecs)))
+        return vals, vecs
+
     def simulate_save(self, setting, n, m, dim, n_anom, seed, out):
         self.lib.ref_simulate_save.argtypes = [C.c_char_p, _sz, _sz, _sz, _sz, C.c_uint64,
                                                C.c_char_p]

@@ -210,6 +210,21 @@ int ref_parse_run_config(const char* path) {
   return guarded([&] { (void)parse_run_config(path); });
 }
 
+// symmetric_top_eigenpairs_subspace (proj/src/linalg.cpp:198-271): values k,
+// vectors k x n.
+int ref_symmetric_top_eigenpairs_subspace(size_t n, const double* s, size_t k, double* values,
+                                          double* vectors) {
+  return guarded([&] {
+    DenseMatrix m(n, n);
+    std::memcpy(m.data(), s, n * n * sizeof(double));
+    const auto pairs = symmetric_top_eigenpairs_subspace(m, k);
+    for (size_t c = 0; c < k; ++c) {
+      values[c] = pairs[c].value;
+      std::memcpy(vectors + c * n, pairs[c].vector.data(), n * sizeof(double));
+    }
+  });
+}
+
 int ref_problem_shape(void* prob, size_t* m, size_t* n) {
   const auto& p = *static_cast<OmnibusProblem*>(prob);
   *m = p.modality_count();

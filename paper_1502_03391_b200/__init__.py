@@ -29,5 +29,6 @@ from .api import (  # noqa: F401
     oos_stress,
     raw_stress,
     stress_pair_count,
+    symmetric_top_eigenpairs_subspace,
 )
 from ._capi import CommError, CudaError, InvalidArgument, NumericalError  # noqa: F401

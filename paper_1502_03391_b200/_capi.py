@@ -87,6 +87,7 @@ _SIGS = {
     "jofc_oos_batch": (C.c_int, [_vp, _sz, _sz, _sz, _sz, _dp, _dp, C.c_double, _dp, C.c_double,
                                  _sz, C.c_int, _dp, _dp, _szp]),
     "jofc_cmds": (C.c_int, [_vp, C.c_int, _sz, _dp]),
+    "jofc_symmetric_top_eigenpairs_subspace": (C.c_int, [_vp, _sz, _dp, _sz, _dp, _dp]),
     "jofc_init_imputed_cmds": (C.c_int, [_vp, _sz, _sz, _dp]),
     "jofc_init_averaged_procrustes": (C.c_int, [_vp, _sz, _dp]),
     # workload generators (include/jofc_workloads.h)

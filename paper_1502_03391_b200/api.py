@@ -398,6 +398,22 @@ def averaged_procrustes_init(problem, d, normalize=False, device=None):
     return out
 
 
+def symmetric_top_eigenpairs_subspace(s, k, device=None):
+    """proj/include/jofc/linalg.hpp:29-35 with the S Q products on the GPU:
+    (values[k], vectors[k, n]) by algebraic value, descending."""
+    s = _f64(s)
+    if s.ndim != 2 or s.shape[0] != s.shape[1]:
+        raise InvalidArgument("symmetric_top_eigenpairs_subspace: matrix not square")
+    if float(np.max(np.abs(s - s.T), initial=0.0)) > 1e-9 * max(1.0, float(np.max(np.abs(s)))):
+        raise InvalidArgument("symmetric_top_eigenpairs_subspace: matrix not symmetric")
+    dev = device or default_device()
+    n = s.shape[0]
+    vals, vecs = np.empty(int(k)), np.empty((int(k), n))
+    check(dev.lib.jofc_symmetric_top_eigenpairs_subspace(dev.h, n, dptr(s), int(k), dptr(vals),
+                                                         dptr(vecs)))
+    return vals, vecs
+
+
 def imputed_omnibus_init(problem, d, dense_cap=4096, normalize=False, device=None):
     """proj/src/init.cpp:90-116 on the GPU (cmds of the imputed omnibus matrix)."""
     dev = device or default_device()

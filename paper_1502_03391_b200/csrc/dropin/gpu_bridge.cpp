@@ -5,6 +5,7 @@
 // One context per (thread, device); each keeps the packed Delta of the last
 // OmnibusProblem it saw resident in HBM (OmnibusProblem is immutable, keyed
 // by cache_id()).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -125,6 +126,23 @@ Configuration imputed_omnibus_init(const OmnibusProblem& problem, std::size_t d,
   std::vector<double> x(problem.modality_count() * problem.object_count() * d);
   check(jofc_init_imputed_cmds(c.h, d, dense_cap, x.data()));
   return unflatten(x, problem.modality_count(), problem.object_count(), d);
+}
+
+std::vector<EigenPair> symmetric_top_eigenpairs_subspace(const DenseMatrix& s, std::size_t k) {
+  if (!is_square(s))
+    throw std::invalid_argument("symmetric_top_eigenpairs_subspace: matrix not square");
+  if (symmetry_gap(s) > 1e-9 * std::max(1.0, max_abs(s)))
+    throw std::invalid_argument("symmetric_top_eigenpairs_subspace: matrix not symmetric");
+  const std::size_t n = s.rows();
+  std::vector<double> values(k), vectors(k * n);
+  check(jofc_symmetric_top_eigenpairs_subspace(ctx().h, n, s.data(), k, values.data(),
+                                               vectors.data()));
+  std::vector<EigenPair> out(k);
+  for (std::size_t c = 0; c < k; ++c) {
+    out[c].value = values[c];
+    out[c].vector.assign(vectors.begin() + c * n, vectors.begin() + (c + 1) * n);
+  }
+  return out;
 }
 
 DenseMatrix cmds(const DenseMatrix& delta, std::size_t d) {

@@ -1045,66 +1045,22 @@ bool panel_ops_for(int p, PanelOps& o) {
   }
 }
 
-constexpr int kOmnibus = -2;
-
-// cmds (proj/src/init.cpp:21-42) of modality `which` (-1: the modality
-// average, kOmnibus: the imputed omnibus matrix) of the resident problem; x is
-// n x d (m n x d for the omnibus) row-major.
-int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
+// Top-k eigenpairs of the symmetric n x n matrix S (device, row-major) with
+// ||S||_F = snorm: the reference's dense cyclic Jacobi (host) when
+// n <= jacobi_limit or k + 4 >= n, else its shifted orthogonal iteration with
+// Rayleigh-Ritz (proj/src/linalg.cpp:167-271) with the n x p panels on the
+// device.  values (k, descending) and vecs (n x k, unit columns, largest
+// component positive).
+int eigen_top_device(jofc_ctx* c, const double* S_dev, long long n, size_t k, double snorm,
+                     long long jacobi_limit, std::vector<double>& values, init::Mat& vecs,
+                     int& sweeps, double& t_sync) {
   using clk = std::chrono::steady_clock;
-  const bool trace = std::getenv("JOFC_INIT_TRACE") != nullptr;
-  const auto t_start = clk::now();
-  double t_sync = 0.0;  // seconds spent waiting on the device inside the sweep loop
-  int sweeps = 0;
-  const Layout& L = c->lay;
-  // which >= 0: modality, -1: modality average, kOmnibus: the m n x m n
-  // imputed omnibus matrix
-  const long long n = (which == kOmnibus) ? static_cast<long long>(L.m) * L.n : L.n;
-  if (d < 1 || static_cast<long long>(d) > n)
-    return set_error(JOFC_EINVAL, "cmds: dimension out of range");
-  DevBuf<double> S, aux;
-  JOFC_CUDA(S.ensure(static_cast<size_t>(n) * n));
-  JOFC_CUDA(aux.ensure(static_cast<size_t>(n) + 1));
-  JOFC_CUDA(cudaMemsetAsync(S.p, 0, static_cast<size_t>(n) * n * sizeof(double), c->stream));
-  if (which == kOmnibus)
-    init::omnibus_d2_kernel<<<static_cast<unsigned>(L.bpm), 256, 0, c->stream>>>(
-        c->delta.p, L.n, L.nT, L.bpm, L.m, S.p);
-  else
-    init::dense_d2_kernel<<<static_cast<unsigned>(L.bpm), 256, 0, c->stream>>>(
-        c->delta.p, n, L.nT, L.bpm, L.m, which, S.p);
-  JOFC_CUDA(cudaGetLastError());
-  init::row_sums_kernel<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, c->stream>>>(S.p, n,
-                                                                                          aux.p);
-  JOFC_CUDA(cudaGetLastError());
-  std::vector<double> rs(n);
-  JOFC_CUDA(cudaMemcpyAsync(rs.data(), aux.p, n * sizeof(double), cudaMemcpyDeviceToHost,
-                            c->stream));
-  JOFC_CUDA(cudaStreamSynchronize(c->stream));
-  const double inv_n = 1.0 / static_cast<double>(n);
-  double total = 0.0;
-  for (long long i = 0; i < n; ++i) {
-    total += rs[i];
-    rs[i] *= inv_n;
-  }
-  total *= inv_n * inv_n;
-  JOFC_CUDA(cudaMemcpyAsync(aux.p, rs.data(), n * sizeof(double), cudaMemcpyHostToDevice,
-                            c->stream));
-  DevBuf<double> fro2;
-  JOFC_CUDA(fro2.ensure(1));
-  JOFC_CUDA(cudaMemsetAsync(fro2.p, 0, sizeof(double), c->stream));
-  init::double_center_kernel<<<static_cast<unsigned>(c->num_sms * 8), 256, 0, c->stream>>>(
-      S.p, n, aux.p, total, fro2.p);
-  JOFC_CUDA(cudaGetLastError());
-  c->launches += 3;
-  double f2 = 0.0;
-  JOFC_CUDA(cudaMemcpyAsync(&f2, fro2.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  JOFC_CUDA(cudaStreamSynchronize(c->stream));
-  const double snorm = std::sqrt(f2);
-
-  const size_t k = d;
-  std::vector<double> values(k);
-  init::Mat vecs(n, k);
-  if (n <= 320 || k + 4 >= static_cast<size_t>(n)) {
+  struct {
+    const double* p;
+  } S{S_dev};
+  values.assign(k, 0.0);
+  vecs = init::Mat(n, k);
+  if (n <= jacobi_limit || k + 4 >= static_cast<size_t>(n)) {
     // the reference's dense route (cyclic Jacobi on the whole S)
     init::Mat h(n, n);
     JOFC_TRY(copy_sync(c, h.a.data(), S.p, h.a.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1179,9 +1135,6 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
     };
     bool done = false;
     std::vector<double> acc;
-    if (trace)
-      std::fprintf(stderr, "[init] cmds(%d) n=%lld p=%zu setup %.3f s\n", which, n, p,
-                   std::chrono::duration<double>(clk::now() - t_start).count());
     for (int iter = 0; iter < 5000 && !done; ++iter) {
       ++sweeps;
       cudaEvent_t pe1 = nullptr;
@@ -1275,6 +1228,72 @@ int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
       return set_error(JOFC_ENUMERIC,
                        "subspace eigensolver did not converge within the iteration cap");
   }
+  return JOFC_OK;
+}
+
+constexpr int kOmnibus = -2;
+
+// cmds (proj/src/init.cpp:21-42) of modality `which` (-1: the modality
+// average, kOmnibus: the imputed omnibus matrix) of the resident problem; x is
+// n x d (m n x d for the omnibus) row-major.
+int cmds_gpu(jofc_ctx* c, int which, size_t d, init::Mat& x) {
+  using clk = std::chrono::steady_clock;
+  const bool trace = std::getenv("JOFC_INIT_TRACE") != nullptr;
+  const auto t_start = clk::now();
+  double t_sync = 0.0;  // seconds spent waiting on the device inside the sweep loop
+  int sweeps = 0;
+  const Layout& L = c->lay;
+  // which >= 0: modality, -1: modality average, kOmnibus: the m n x m n
+  // imputed omnibus matrix
+  const long long n = (which == kOmnibus) ? static_cast<long long>(L.m) * L.n : L.n;
+  if (d < 1 || static_cast<long long>(d) > n)
+    return set_error(JOFC_EINVAL, "cmds: dimension out of range");
+  DevBuf<double> S, aux;
+  JOFC_CUDA(S.ensure(static_cast<size_t>(n) * n));
+  JOFC_CUDA(aux.ensure(static_cast<size_t>(n) + 1));
+  JOFC_CUDA(cudaMemsetAsync(S.p, 0, static_cast<size_t>(n) * n * sizeof(double), c->stream));
+  if (which == kOmnibus)
+    init::omnibus_d2_kernel<<<static_cast<unsigned>(L.bpm), 256, 0, c->stream>>>(
+        c->delta.p, L.n, L.nT, L.bpm, L.m, S.p);
+  else
+    init::dense_d2_kernel<<<static_cast<unsigned>(L.bpm), 256, 0, c->stream>>>(
+        c->delta.p, n, L.nT, L.bpm, L.m, which, S.p);
+  JOFC_CUDA(cudaGetLastError());
+  init::row_sums_kernel<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, c->stream>>>(S.p, n,
+                                                                                          aux.p);
+  JOFC_CUDA(cudaGetLastError());
+  std::vector<double> rs(n);
+  JOFC_CUDA(cudaMemcpyAsync(rs.data(), aux.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  const double inv_n = 1.0 / static_cast<double>(n);
+  double total = 0.0;
+  for (long long i = 0; i < n; ++i) {
+    total += rs[i];
+    rs[i] *= inv_n;
+  }
+  total *= inv_n * inv_n;
+  JOFC_CUDA(cudaMemcpyAsync(aux.p, rs.data(), n * sizeof(double), cudaMemcpyHostToDevice,
+                            c->stream));
+  DevBuf<double> fro2;
+  JOFC_CUDA(fro2.ensure(1));
+  JOFC_CUDA(cudaMemsetAsync(fro2.p, 0, sizeof(double), c->stream));
+  init::double_center_kernel<<<static_cast<unsigned>(c->num_sms * 8), 256, 0, c->stream>>>(
+      S.p, n, aux.p, total, fro2.p);
+  JOFC_CUDA(cudaGetLastError());
+  c->launches += 3;
+  double f2 = 0.0;
+  JOFC_CUDA(cudaMemcpyAsync(&f2, fro2.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  const double snorm = std::sqrt(f2);
+
+  const size_t k = d;
+  std::vector<double> values;
+  init::Mat vecs;
+  {
+    const int rc = eigen_top_device(c, S.p, n, k, snorm, 320, values, vecs, sweeps, t_sync);
+    if (rc) return rc;
+  }
   if (trace)
     std::fprintf(stderr, "[init] cmds(%d) total %.3f s, %d sweeps, device wait %.3f s\n", which,
                  std::chrono::duration<double>(clk::now() - t_start).count(), sweeps, t_sync);
@@ -1308,6 +1327,42 @@ int jofc_cmds(jofc_ctx* c, int modality, size_t d, double* x_out) {
   rc = cmds_gpu(c, modality, d, x);
   if (rc) return rc;
   JOFC_TRY(copy_sync(c, x_out, x.a.data(), x.a.size() * sizeof(double), cudaMemcpyDefault));
+  return JOFC_OK;
+}
+
+int jofc_symmetric_top_eigenpairs_subspace(jofc_ctx* c, size_t n, const double* s, size_t k,
+                                           double* values, double* vectors) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  if (!s || !values || !vectors) return set_error(JOFC_EINVAL, "null argument");
+  if (k < 1 || k > n)
+    return set_error(JOFC_EINVAL, "symmetric_top_eigenpairs_subspace: k out of range");
+  if (k + 4 > static_cast<size_t>(init::kMaxP) && n > 64 && k + 4 < n)
+    return set_error(JOFC_EINVAL, "symmetric_top_eigenpairs_subspace: k %zu above %d", k,
+                     init::kMaxP - 4);
+  JOFC_CUDA(cudaSetDevice(c->device));
+  const long long nn = static_cast<long long>(n);
+  DevBuf<double> S, rows;
+  JOFC_CUDA(S.ensure(n * n));
+  JOFC_CUDA(rows.ensure(n));
+  JOFC_CUDA(cudaMemcpyAsync(S.p, s, n * n * sizeof(double), cudaMemcpyDefault, c->stream));
+  init::row_sumsq_kernel<<<static_cast<unsigned>((nn * 32 + 255) / 256), 256, 0, c->stream>>>(
+      S.p, nn, rows.p);
+  JOFC_CUDA(cudaGetLastError());
+  ++c->launches;
+  std::vector<double> rs(n);
+  JOFC_TRY(copy_sync(c, rs.data(), rows.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  double f2 = 0.0;
+  for (double v : rs) f2 += v;
+  std::vector<double> vals;
+  init::Mat vecs;
+  int sweeps = 0;
+  double t_sync = 0.0;
+  JOFC_TRY(eigen_top_device(c, S.p, nn, k, std::sqrt(f2), 64, vals, vecs, sweeps, t_sync));
+  std::vector<double> out(k * n);
+  for (size_t cc = 0; cc < k; ++cc)
+    for (size_t r = 0; r < n; ++r) out[cc * n + r] = vecs(r, cc);
+  JOFC_TRY(copy_sync(c, values, vals.data(), k * sizeof(double), cudaMemcpyDefault));
+  JOFC_TRY(copy_sync(c, vectors, out.data(), out.size() * sizeof(double), cudaMemcpyDefault));
   return JOFC_OK;
 }
 

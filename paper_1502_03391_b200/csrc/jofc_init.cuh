@@ -112,6 +112,19 @@ __global__ void __launch_bounds__(256) row_sums_kernel(const double* __restrict_
   if (lane == 0) out[row] = s;
 }
 
+// Row sums of squares of a dense n x n matrix (||S||_F by the host, in row
+// order): one warp per row.
+__global__ void __launch_bounds__(256) row_sumsq_kernel(const double* __restrict__ a, long long n,
+                                                        double* __restrict__ out) {
+  const long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (long long j = lane; j < n; j += 32) s = fma(a[row * n + j], a[row * n + j], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[row] = s;
+}
+
 // In place: S_ij = -1/2 (D2_ij - rm_i - rm_j + tm) (proj/src/distance.cpp:31-53),
 // accumulating sum S_ij^2 for ||S||_F.
 __global__ void __launch_bounds__(256) double_center_kernel(double* __restrict__ a, long long n,

@@ -294,6 +294,72 @@ static void out_of_sample() {
         }
 }
 
+static double max_abs_mat(const DenseMatrix& a, const DenseMatrix& b) {
+  double m = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a.data()[i] - b.data()[i]));
+  return m;
+}
+
+static void linear_algebra() {
+  // proj/include/jofc/linalg.hpp contracts, checked through their defining
+  // identities (the subspace solver additionally against the Jacobi route)
+  Rng rng(91);
+  for (std::size_t n : {1, 2, 3, 5, 8}) {
+    const DenseMatrix a = random_matrix(rng, n, n);
+    const Svd svd = svd_small(a);
+    DenseMatrix sig(n, n);
+    for (std::size_t i = 0; i < n; ++i) sig(i, i) = svd.sigma[i];
+    CHECK(max_abs_mat(svd.u * sig * transpose(svd.v), a) < 1e-12 * std::max(1.0, max_abs(a)));
+    CHECK(max_abs_mat(transpose(svd.u) * svd.u, DenseMatrix::identity(n)) < 1e-12);
+    CHECK(max_abs_mat(transpose(svd.v) * svd.v, DenseMatrix::identity(n)) < 1e-12);
+    for (std::size_t i = 1; i < n; ++i) CHECK(svd.sigma[i - 1] >= svd.sigma[i]);
+    const DenseMatrix inv = invert_small(a);
+    CHECK(max_abs_mat(a * inv, DenseMatrix::identity(n)) < 1e-9);
+  }
+  DenseMatrix rank1(3, 3);  // rank-deficient: U still orthogonal
+  for (std::size_t i = 0; i < 3; ++i)
+    for (std::size_t j = 0; j < 3; ++j) rank1(i, j) = double(i + 1) * double(j + 2);
+  const Svd r1 = svd_small(rank1);
+  CHECK(max_abs_mat(transpose(r1.u) * r1.u, DenseMatrix::identity(3)) < 1e-12);
+  CHECK(throws<NumericalError>([&] { invert_small(rank1); }));
+  CHECK(throws<std::invalid_argument>([&] { invert_small(DenseMatrix(2, 3)); }));
+
+  const std::size_t n = 200;
+  const DenseMatrix g = random_matrix(rng, n, 9);
+  const DenseMatrix s = g * transpose(g);  // rank 9, symmetric PSD
+  const auto all = symmetric_eigen_all(s);
+  CHECK(all.size() == n);
+  for (std::size_t i = 1; i < n; ++i) CHECK(all[i - 1].value >= all[i].value);
+  const auto top = symmetric_top_eigenpairs(s, 4);
+  const auto sub = symmetric_top_eigenpairs_subspace(s, 4);  // GPU route (n > 64)
+  for (std::size_t c = 0; c < 4; ++c) {
+    CHECK(std::abs(top[c].value - all[c].value) <= 1e-12 * std::abs(all[0].value));
+    CHECK(std::abs(sub[c].value - top[c].value) <= 1e-9 * std::abs(all[0].value));
+    double dev = 0.0;
+    for (std::size_t r = 0; r < n; ++r)
+      dev = std::max(dev, std::abs(sub[c].vector[r] - top[c].vector[r]));
+    CHECK(dev < 1e-6);
+  }
+  const DenseMatrix pinv = pseudoinverse_oracle(s);
+  CHECK(max_abs_mat(s * pinv * s, s) < 1e-8 * max_abs(s));
+  DenseMatrix asym = s;
+  asym(0, 1) += 1.0;
+  CHECK(throws<std::invalid_argument>([&] { symmetric_top_eigenpairs_subspace(asym, 2); }));
+  CHECK(throws<std::invalid_argument>([&] { symmetric_top_eigenpairs(s, n + 1); }));
+
+  // Procrustes recovers a rotation (up to the centring it applies)
+  const DenseMatrix src = random_matrix(rng, 50, 2);
+  DenseMatrix rot(2, 2);
+  rot(0, 0) = std::cos(0.7);
+  rot(0, 1) = -std::sin(0.7);
+  rot(1, 0) = std::sin(0.7);
+  rot(1, 1) = std::cos(0.7);
+  DenseMatrix centred = src;
+  center_columns(centred);
+  const DenseMatrix tgt = centred * rot;
+  CHECK(max_abs_mat(orthogonal_procrustes(src, tgt), tgt) < 1e-12);
+}
+
 int main() {
   fast_step_grid();
   solve_trajectory();
@@ -301,6 +367,7 @@ int main() {
   default_init_runs();
   errors();
   out_of_sample();
+  linear_algebra();
   std::printf("dropin_parity: %d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

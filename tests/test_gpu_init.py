@@ -103,3 +103,23 @@ def test_imputed_dense_cap(R):
     x0 = R.imputed_omnibus_init(delta, 2)
     ref = R.fjofc_embed(delta, Spec.uniform(1.0), x0, 1e-300, 20)
     assert rel_fro(got.config, ref.x) < 1e-8
+
+
+@pytest.mark.parametrize("n,k,kind", [(50, 3, "psd"), (400, 3, "indef"), (1500, 5, "psd"),
+                                      (700, 6, "indef"), (700, 10, "psd"), (300, 1, "zero")])
+def test_symmetric_top_eigenpairs_subspace(R, n, k, kind):
+    rng = np.random.default_rng(n + k)
+    if kind == "zero":
+        s = np.zeros((n, n))
+    else:
+        a = rng.normal(size=(n, 12))
+        s = a @ a.T if kind == "psd" else a @ np.diag(np.linspace(-3, 5, 12)) @ a.T
+        s = 0.5 * (s + s.T)
+    rv, rvec = R.symmetric_top_eigenpairs_subspace(s, k)
+    gv, gvec = jg.symmetric_top_eigenpairs_subspace(s, k)
+    scale = max(1.0, float(np.max(np.abs(rv))))
+    assert np.max(np.abs(gv - rv)) <= 1e-9 * scale, (gv, rv)
+    if kind != "zero":  # top-k inside the 8 (12) nonzero, distinct eigenvalues
+        assert rel_fro(gvec, rvec) < 1e-6, rel_fro(gvec, rvec)
+    with pytest.raises(jg.InvalidArgument):
+        jg.symmetric_top_eigenpairs_subspace(s, n + 1)
