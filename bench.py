@@ -132,8 +132,8 @@ def h2d_bytes_dense_upload(m, n, world, rank):
         return B * nT - B * (B - 1)
 
     bpm = rf(nB)
-    total = m * bpm
-    lo, hi = total * rank // world, total * (rank + 1) // world
+    from paper_1502_03391_b200 import layout
+    lo, hi = layout.shard_range(m, n, rank, world)
     b = 0
     for l in range(m):
         for B0 in range(0, nB, K):

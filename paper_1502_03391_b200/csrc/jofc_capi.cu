@@ -144,6 +144,10 @@ struct jofc_ctx {
   DevBuf<Control> ctrl;
   Control* ctrl_host = nullptr;  // pinned
   int pass_grid = 0, epi_grid = 0;
+  // per-CTA stream ranges of the pass kernel (pass_bounds) and what they were
+  // computed for
+  DevBuf<long long> bounds;
+  std::vector<long long> bounds_key;
   size_t max_it_enqueued = 0;
   // caller-owned exchange buffer (multi-GPU) and pass-kernel instrumentation
   double* ext_P = nullptr;
@@ -257,6 +261,24 @@ int require_problem(jofc_ctx* c) {
   return JOFC_OK;
 }
 
+// Estimated pass-kernel cost of one block, in units of an interior block: masked
+// blocks (diagonal-crossing or padded) +0.1, the first block a CTA processes
+// of a row band +band_cost() (flush of the row sums, X row-block staging, two
+// CTA barriers; 1.0 measured best at C3/C4/C5 among 0, 0.5, 1, 1.5, 2, 4, 8).
+double band_cost() {
+  static const double v = [] {
+    const char* e = std::getenv("JOFC_BAND_COST");  // experiments
+    return e ? std::atof(e) : 1.0;
+  }();
+  return v;
+}
+
+double block_cost(const Layout& L, int B, int J, bool enters_band) {
+  const bool masked = J <= 2 * B + 1 || static_cast<long long>(kCols) * (J + 1) > L.n ||
+                      static_cast<long long>(kRows) * (B + 1) > L.n;
+  return 1.0 + (masked ? 0.1 : 0.0) + (enters_band ? band_cost() : 0.0);
+}
+
 // Layout for m modalities of n objects; this shard's contiguous stream range.
 void make_layout(jofc_ctx* c, size_t m, size_t n) {
   Layout& L = c->lay;
@@ -267,8 +289,70 @@ void make_layout(jofc_ctx* c, size_t m, size_t n) {
   L.n_pad = static_cast<long long>(L.nB) * kRows;
   L.bpm = blocks_per_modality(L.nT);
   const long long total = L.total();
-  L.begin = total * c->rank / c->world;
-  L.end = total * (c->rank + 1) / c->world;
+  if (c->world == 1) {
+    L.begin = 0;
+    L.end = total;
+    return;
+  }
+  // shards: contiguous slices of equal estimated cost (block_cost; the same
+  // model the CTA ranges use), identical on every rank
+  std::vector<double> cost;
+  cost.reserve(static_cast<size_t>(total));
+  for (int l = 0; l < L.m; ++l)
+    for (int B = 0; B < L.nB; ++B)
+      for (int J = 2 * B; J < L.nT; ++J) cost.push_back(block_cost(L, B, J, J == 2 * B));
+  double sum = 0.0;
+  for (double v : cost) sum += v;
+  long long cut_lo = 0, cut_hi = total;
+  double acc = 0.0;
+  for (long long g = 0; g < total; ++g) {
+    acc += cost[g];
+    if (c->rank > 0 && cut_lo == 0 && acc >= sum * c->rank / c->world) cut_lo = g + 1;
+    if (acc >= sum * (c->rank + 1) / c->world && c->rank + 1 < c->world) {
+      cut_hi = g + 1;
+      break;
+    }
+  }
+  L.begin = cut_lo;
+  L.end = cut_hi;
+}
+
+// CTA ranges of the pass kernel: contiguous slices of this shard's block
+// stream with equal estimated cost (block_cost).  With equal block counts the
+// CTAs holding the short bands at the end of the stream ran ~6% longer than
+// the average (ncu: SM active 93.8% of elapsed); balanced, the C3 pass is 5.7%
+// faster, C4 4.6%, C5 13%.
+int pass_bounds(jofc_ctx* c) {
+  const Layout& L = c->lay;
+  const std::vector<long long> key = {L.begin, L.end, L.nT, L.n, c->pass_grid,
+                                      static_cast<long long>(band_cost() * 1000)};
+  if (key == c->bounds_key && c->bounds.p) return JOFC_OK;
+  const int NG = c->pass_grid;
+  std::vector<double> cost;
+  cost.reserve(static_cast<size_t>(L.local()));
+  long long g = 0;
+  for (int l = 0; l < L.m; ++l)
+    for (int B = 0; B < L.nB; ++B)
+      for (int J = 2 * B; J < L.nT; ++J, ++g) {
+        if (g < L.begin || g >= L.end) continue;
+        cost.push_back(block_cost(L, B, J, J == 2 * B || g == L.begin));
+      }
+  double total = 0.0;
+  for (double v : cost) total += v;
+  std::vector<long long> b(NG + 1, L.end);
+  b[0] = L.begin;
+  double acc = 0.0;
+  int cut = 1;
+  for (size_t i = 0; i < cost.size() && cut < NG; ++i) {
+    acc += cost[i];
+    if (acc >= total * cut / NG) b[cut++] = L.begin + static_cast<long long>(i) + 1;
+  }
+  for (; cut < NG; ++cut) b[cut] = L.end;
+  JOFC_CUDA(c->bounds.ensure(NG + 1));
+  JOFC_TRY(copy_sync(c, c->bounds.p, b.data(), (NG + 1) * sizeof(long long),
+                     cudaMemcpyHostToDevice));
+  c->bounds_key = key;
+  return JOFC_OK;
 }
 
 int alloc_solve_state(jofc_ctx* c, size_t d, size_t max_it) {
@@ -286,6 +370,7 @@ int alloc_solve_state(jofc_ctx* c, size_t d, size_t max_it) {
   c->pass_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(c->num_sms, L.local())));
   c->epi_grid = static_cast<int>((L.n + 255) / 256);
   JOFC_CUDA(c->fid_part.ensure(c->pass_grid));
+  JOFC_TRY(pass_bounds(c));
   JOFC_CUDA(c->com_part.ensure(c->epi_grid));
   JOFC_CUDA(c->trace.ensure(max_it + 1));
   JOFC_CUDA(c->ctrl.ensure(1));
@@ -370,6 +455,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   pp.begin = L.begin;
   pp.end = L.end;
   pp.fid_slot = fid_slot(c);
+  pp.bounds = c->bounds.p;
   {
     const char* dg = getenv("JOFC_DIAG");  // experiments only; results are wrong when set
     pp.diag = dg ? atoi(dg) : 0;

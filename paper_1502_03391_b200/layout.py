@@ -3,7 +3,8 @@
 Used by the sharding plan, bench.py's byte accounting and the CPU tests of
 the multi-GPU partition.  Row blocks of 128 rows x column tiles of 64 columns,
 block (B, J) stored for J >= 2B, stream order (modality, B, J); a shard owns
-a balanced contiguous range of the stream.
+a contiguous range of the stream of equal estimated pass-kernel cost
+(block_cost, the model of csrc/jofc_capi.cu: make_layout / pass_bounds).
 """
 from __future__ import annotations
 
@@ -35,11 +36,36 @@ def block_coords(g, nT, bpm):
     return l, B, 2 * B + (r - row_first(nT, B))
 
 
+BAND_COST = 1.0  # a row band entered: flush, X row-block staging, two CTA barriers
+MASK_COST = 0.1  # diagonal-crossing or padded block (masked pairs)
+
+
+def block_cost(n, B, J, enters_band):
+    masked = J <= 2 * B + 1 or COLS * (J + 1) > n or ROWS * (B + 1) > n
+    return 1.0 + (MASK_COST if masked else 0.0) + (BAND_COST if enters_band else 0.0)
+
+
 def shard_range(m, n, rank, world):
-    """[begin, end) stream indices owned by `rank` (balanced by block count)."""
-    _, _, bpm = geometry(n)
+    """[begin, end) stream indices owned by `rank`: equal estimated cost, the
+    same cut (same summation order) as make_layout in csrc/jofc_capi.cu."""
+    nT, nB, bpm = geometry(n)
     total = m * bpm
-    return total * rank // world, total * (rank + 1) // world
+    if world == 1:
+        return 0, total
+    cost = [block_cost(n, B, J, J == 2 * B)
+            for _ in range(m) for B in range(nB) for J in range(2 * B, nT)]
+    s = 0.0
+    for v in cost:
+        s += v
+    lo, hi, acc = 0, total, 0.0
+    for g, v in enumerate(cost):
+        acc += v
+        if rank > 0 and lo == 0 and acc >= s * rank / world:
+            lo = g + 1
+        if acc >= s * (rank + 1) / world and rank + 1 < world:
+            hi = g + 1
+            break
+    return lo, hi
 
 
 def blocks(m, n, rank=0, world=1):

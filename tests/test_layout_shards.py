@@ -1,7 +1,7 @@
 """Packed layout and multi-GPU sharding, host side (CPU).
 
 * the stream enumerates every upper-triangle pair exactly once;
-* shard ranges partition the stream and balance block counts;
+* shard ranges partition the stream and balance the estimated cost;
 * a world_size-2 gloo run: each rank forms the partial B(X)X products and
   fidelity of ITS blocks only (numpy emulation of the pass kernel's
   arithmetic contract), all-reduces them, applies the W^-1 mix, and must
@@ -37,8 +37,14 @@ def test_shards_partition_and_balance(world):
     assert ranges[0][0] == 0 and ranges[-1][1] == m * layout.geometry(n)[2]
     for a, b in zip(ranges, ranges[1:]):
         assert a[1] == b[0]
-    sizes = [hi - lo for lo, hi in ranges]
-    assert max(sizes) - min(sizes) <= 1
+    # balanced by estimated cost (block_cost), not block count: no shard more
+    # than one block's (+ one band entry's) cost above the mean
+    nT, nB, _ = layout.geometry(n)
+    cost = [layout.block_cost(n, B, J, J == 2 * B)
+            for _ in range(m) for B in range(nB) for J in range(2 * B, nT)]
+    shares = [sum(cost[lo:hi]) for lo, hi in ranges]
+    mean = sum(cost) / world
+    assert max(shares) - mean <= 1.0 + layout.MASK_COST + layout.BAND_COST
 
 
 def partial_products(delta, x, within, m, n, rank, world):
