@@ -1,0 +1,173 @@
+// capi_internal.h -- what the translation units of libjofc_gpu.so share:
+// the context struct, error plumbing, device buffers and the small helpers
+// (jofc_capi.cu: context, solve, stress, step, out-of-sample; capi_init.cu:
+// the initialisers and the eigen-solver; capi_ingest.cu: file ingest).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "jofc_gpu.h"
+#include "jofc_kernels.cuh"
+#include "jofc_oos.cuh"
+
+namespace jofc_gpu {
+namespace capi {
+
+inline thread_local std::string g_error;
+
+inline int set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_error = buf;
+  return code;
+}
+
+#define JOFC_CUDA(call)                                                                 \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_error(JOFC_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                       __FILE__, __LINE__);                                             \
+  } while (0)
+
+#define JOFC_TRY(call)     \
+  do {                     \
+    const int rc_ = (call); \
+    if (rc_) return rc_;   \
+  } while (0)
+
+constexpr int kMaxD = 10;
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// Double-buffered staging of streaming ingest (kept across loads): pinned
+// host panels, their copy-done events, and the device panels.
+struct IngestPanels {
+  double* host[2] = {nullptr, nullptr};
+  size_t cap = 0;  // doubles per panel
+  cudaEvent_t copied[2] = {nullptr, nullptr};
+  DevBuf<double> stage[2];
+  void release() {
+    for (int k = 0; k < 2; ++k) {
+      if (host[k]) cudaFreeHost(host[k]);
+      if (copied[k]) cudaEventDestroy(copied[k]);
+      host[k] = nullptr;
+      copied[k] = nullptr;
+      stage[k].release();
+    }
+    cap = 0;
+  }
+  cudaError_t ensure(size_t doubles) {
+    if (doubles <= cap) return cudaSuccess;
+    release();
+    for (int k = 0; k < 2; ++k) {
+      cudaError_t e = cudaMallocHost(&host[k], doubles * sizeof(double));
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = stage[k].ensure(doubles);
+      if (e != cudaSuccess) {
+        release();
+        return e;
+      }
+    }
+    cap = doubles;
+    return cudaSuccess;
+  }
+};
+
+}  // namespace capi
+}  // namespace jofc_gpu
+
+// The opaque handle of include/jofc_gpu.h.
+struct jofc_ctx {
+  template <class T>
+  using DevBuf = jofc_gpu::capi::DevBuf<T>;
+  using IngestPanels = jofc_gpu::capi::IngestPanels;
+  using Layout = jofc_gpu::Layout;
+  using Control = jofc_gpu::Control;
+  using OosPoint = jofc_gpu::OosPoint;
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  // sharding / exchange
+  int rank = 0, world = 1;
+  jofc_allreduce_fn allreduce = nullptr;
+  void* allreduce_user = nullptr;
+  // problem
+  bool has_problem = false;
+  Layout lay;
+  DevBuf<double> delta;
+  // solve state (sized for the current d)
+  size_t d = 0;
+  DevBuf<double> x0, x1, P, fid_part, com_part, trace, consts;
+  DevBuf<Control> ctrl;
+  Control* ctrl_host = nullptr;  // pinned
+  int pass_grid = 0, epi_grid = 0;
+  // per-CTA stream ranges of the pass kernel (pass_bounds) and what they were
+  // computed for
+  DevBuf<long long> bounds;
+  std::vector<long long> bounds_key;
+  size_t max_it_enqueued = 0;
+  // caller-owned exchange buffer (multi-GPU) and pass-kernel instrumentation
+  double* ext_P = nullptr;
+  size_t ext_cap = 0;
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  size_t prof_used = 0;
+  // CUDA graph of the whole launch sequence (single-GPU, no events)
+  std::map<std::vector<uintptr_t>, cudaGraphExec_t> graphs;
+  bool use_graphs = true;
+  // oos state
+  DevBuf<double> oos_x, oos_delta, oos_y0, oos_y1, oos_part, oos_trace;
+  DevBuf<OosPoint> oos_st;
+  // streaming ingest staging
+  IngestPanels ingest;
+  // host -> device upload: copies on their own stream, overlapped with packing
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t up_copied[2] = {nullptr, nullptr}, up_packed[2] = {nullptr, nullptr};
+};
+
+namespace jofc_gpu {
+namespace capi {
+
+int copy_sync(jofc_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
+int prof_begin(jofc_ctx* c, cudaEvent_t* end);
+int require_problem(jofc_ctx* c);
+double band_cost();
+double block_cost(const Layout& L, int B, int J, bool enters_band);
+void make_layout(jofc_ctx* c, size_t m, size_t n);
+
+}  // namespace capi
+}  // namespace jofc_gpu

@@ -39,7 +39,7 @@ namespace init {
 // modality average when which < 0 (sum in modality order, then / m, as
 // proj/src/init.cpp:62-67), squared (proj/src/init.cpp:26-28).  The diagonal
 // is left to a prior memset.
-__global__ void __launch_bounds__(256) dense_d2_kernel(const double* __restrict__ packed,
+static __global__ void __launch_bounds__(256) dense_d2_kernel(const double* __restrict__ packed,
                                                        long long n, int nT, long long bpm, int m,
                                                        int which, double* __restrict__ d2) {
   const long long g0 = blockIdx.x;  // block index within one modality
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) dense_d2_kernel(const double* __restrict_
 // 0.5 (Delta_bi + Delta_bj) otherwise (same rounding as the host), each entry
 // then squared as cmds does.  One CTA per packed block of modality 0's stream
 // coordinates; every unordered modality pair writes its four mirror entries.
-__global__ void __launch_bounds__(256) omnibus_d2_kernel(const double* __restrict__ packed,
+static __global__ void __launch_bounds__(256) omnibus_d2_kernel(const double* __restrict__ packed,
                                                          long long n, int nT, long long bpm, int m,
                                                          double* __restrict__ d2) {
   const long long g0 = blockIdx.x;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) omnibus_d2_kernel(const double* __restric
 }
 
 // Row sums of a dense n x n matrix: one warp per row.
-__global__ void __launch_bounds__(256) row_sums_kernel(const double* __restrict__ a, long long n,
+static __global__ void __launch_bounds__(256) row_sums_kernel(const double* __restrict__ a, long long n,
                                                        double* __restrict__ out) {
   const long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) row_sums_kernel(const double* __restrict_
 
 // Row sums of squares of a dense n x n matrix (||S||_F by the host, in row
 // order): one warp per row.
-__global__ void __launch_bounds__(256) row_sumsq_kernel(const double* __restrict__ a, long long n,
+static __global__ void __launch_bounds__(256) row_sumsq_kernel(const double* __restrict__ a, long long n,
                                                         double* __restrict__ out) {
   const long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256) row_sumsq_kernel(const double* __restrict
 
 // In place: S_ij = -1/2 (D2_ij - rm_i - rm_j + tm) (proj/src/distance.cpp:31-53),
 // accumulating sum S_ij^2 for ||S||_F.
-__global__ void __launch_bounds__(256) double_center_kernel(double* __restrict__ a, long long n,
+static __global__ void __launch_bounds__(256) double_center_kernel(double* __restrict__ a, long long n,
                                                             const double* __restrict__ rm,
                                                             double tm, double* __restrict__ fro2) {
   const long long total = n * n;
