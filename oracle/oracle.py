@@ -314,6 +314,21 @@ class Reference:
         finally:
             L.ref_problem_destroy(h)
 
+    def oos_step_reference(self, y, x, deltas, w):
+        y, x, deltas = _f64(y), _f64(x), _f64(deltas)
+        m, n, d = x.shape
+        out = np.empty((m, d))
+        self.lib.ref_oos_step_reference.argtypes = None
+        self._check(self.lib.ref_oos_step_reference(_sz(m), _sz(n), _sz(d), _ptr(y), _ptr(x),
+                                                    _ptr(deltas), C.c_double(w), _ptr(out)))
+        return out
+
+    def generate_matched(self, n, m, dim, seed):
+        out = np.empty((m, n, n))
+        self._check(self.lib.ref_generate_matched(_sz(n), _sz(m), _sz(dim), C.c_uint64(seed),
+                                                  _ptr(out)))
+        return out
+
     def symmetric_top_eigenpairs_subspace(self, s, k):
         s = _f64(s)
         n = s.shape[0]

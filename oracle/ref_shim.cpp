@@ -225,6 +225,34 @@ int ref_symmetric_top_eigenpairs_subspace(size_t n, const double* s, size_t k, d
   });
 }
 
+// oos_step_reference (proj/src/oos.cpp:129-178, the dense OOS transform).
+int ref_oos_step_reference(size_t m, size_t n, size_t d, const double* y, const double* x,
+                           const double* deltas, double w, double* y_out) {
+  return guarded([&] {
+    DenseMatrix ym(m, d);
+    std::memcpy(ym.data(), y, m * d * sizeof(double));
+    Configuration xc;
+    for (size_t l = 0; l < m; ++l) {
+      DenseMatrix b(n, d);
+      std::memcpy(b.data(), x + l * n * d, n * d * sizeof(double));
+      xc.blocks.push_back(std::move(b));
+    }
+    OosDissimilarity od;
+    for (size_t l = 0; l < m; ++l) od.deltas.emplace_back(deltas + l * n, deltas + (l + 1) * n);
+    const DenseMatrix out = oos_step_reference(ym, xc, od, w);
+    std::memcpy(y_out, out.data(), m * d * sizeof(double));
+  });
+}
+
+// generate_matched (proj/src/simulate.cpp): the m dense n x n dissimilarities.
+int ref_generate_matched(size_t n, size_t m, size_t dim, uint64_t seed, double* delta_out) {
+  return guarded([&] {
+    const SimulatedProblem sim = generate_matched(n, m, dim, seed);
+    for (size_t l = 0; l < m; ++l)
+      std::memcpy(delta_out + l * n * n, sim.modalities[l].data(), n * n * sizeof(double));
+  });
+}
+
 int ref_problem_shape(void* prob, size_t* m, size_t* n) {
   const auto& p = *static_cast<OmnibusProblem*>(prob);
   *m = p.modality_count();

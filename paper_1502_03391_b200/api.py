@@ -222,6 +222,7 @@ class EmbeddingResult:
     iterations: int
     terminated: Termination
     step_seconds: list = field(default_factory=list)
+    config_trace: list = field(default_factory=list)
 
     def final_stress(self):
         return self.stress_trace[-1]
@@ -447,6 +448,8 @@ def fjofc_embed(problem, spec, options: SolveOptions, device=None):
         x0 = imputed_omnibus_init(problem, options.dim, options.dense_cap, options.normalize,
                                   device=dev)
     T = int(options.max_iterations)
+    if options.keep_config_trace:
+        return _embed_with_config_trace(problem, spec, options, x0, dev)
     x = np.empty_like(x0)
     trace = np.empty(T + 1)
     steps = np.zeros(max(T, 1))
@@ -462,6 +465,41 @@ def fjofc_embed(problem, spec, options: SolveOptions, device=None):
                            terminated=Termination.converged if conv.value else
                            Termination.max_iterations,
                            step_seconds=steps[:k].tolist())
+
+
+def _embed_with_config_trace(problem, spec, options, x0, dev):
+    """keep_config_trace: the reference loop (proj/src/solver.cpp:106-150)
+    driven from the host, one GPU transform and one GPU stress per iteration,
+    every iterate kept."""
+    m, n = problem.modality_count(), problem.object_count()
+    use = problem.normalized() if options.normalize and not isinstance(
+        problem, ResidentProblem) else problem
+    pairs = stress_pair_count(m, n)
+    x = _f64(x0).copy()
+    stress = raw_stress(x, use, spec, device=dev)
+    if not math.isfinite(stress):
+        raise NumericalError("embed: non-finite stress at the initial configuration")
+    trace, configs, steps = [stress], [x.copy()], []
+    term = Termination.max_iterations
+    for it in range(int(options.max_iterations)):
+        t0 = time.perf_counter()
+        nxt = guttman_step_fast(x, use, spec, device=dev)
+        steps.append(time.perf_counter() - t0)
+        ns = raw_stress(nxt, use, spec, device=dev)
+        if not math.isfinite(ns):
+            raise NumericalError(f"embed: non-finite stress at iteration {it + 1}")
+        x = nxt
+        trace.append(ns)
+        configs.append(x.copy())
+        decrease = (stress - ns) / pairs
+        stress = ns
+        if decrease < options.eps:
+            term = Termination.converged
+            break
+    k = len(trace) - 1
+    return EmbeddingResult(config=x, stress_trace=trace,
+                           normalized_stress_trace=[v / pairs for v in trace], iterations=k,
+                           terminated=term, step_seconds=steps, config_trace=configs)
 
 
 # ------------------------------------------------------------ out-of-sample
