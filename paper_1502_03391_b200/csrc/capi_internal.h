@@ -20,6 +20,9 @@
 namespace jofc_gpu {
 namespace capi {
 
+// Largest n whose epilogue the pass kernel's last CTA runs itself (one GPU).
+constexpr long long kFuseEpilogueMaxN = 1024;
+
 inline thread_local std::string g_error;
 
 inline int set_error(int code, const char* fmt, ...) {

@@ -356,6 +356,17 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   ep.n_pad = L.n_pad;
   ep.fid_slot = fid_slot(c);
 
+  // Small problems on one GPU: the pass kernel's last CTA runs the epilogue
+  // too (one launch per iteration instead of two).  The threshold keeps the
+  // one-CTA epilogue below the cost of a second launch.
+  {
+    const char* e = std::getenv("JOFC_FUSE_EPI_N");  // experiments
+    const long long limit = e ? std::atoll(e) : kFuseEpilogueMaxN;
+    pp.fuse_epilogue = (c->world == 1 && L.n <= limit) ? 1 : 0;
+  }
+  pp.epi = ep;
+  const bool fused = pp.fuse_epilogue != 0;
+
   // Single GPU, no per-launch events: replay a captured CUDA graph of the
   // whole 2(max_it + 1)-kernel sequence (kernel parameters only hold buffer
   // pointers; everything iteration-dependent lives in the control block).
@@ -374,7 +385,8 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
                                   reinterpret_cast<uintptr_t>(ep.coef),
                                   static_cast<uintptr_t>(L.n), static_cast<uintptr_t>(L.m),
                                   static_cast<uintptr_t>(L.begin), static_cast<uintptr_t>(L.end),
-                                  static_cast<uintptr_t>(pp.diag)};
+                                  static_cast<uintptr_t>(pp.diag),
+                                  static_cast<uintptr_t>(pp.fuse_epilogue)};
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       if (c->graphs.size() >= 8) {
@@ -387,7 +399,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
       int lrc = JOFC_OK;
       for (size_t t = 0; t <= max_it && !lrc; ++t) {
         lrc = pass_for_d(c, pp);
-        if (!lrc) lrc = epi_for_d(c, ep);
+        if (!lrc && !fused) lrc = epi_for_d(c, ep);
       }
       cudaGraph_t g = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
@@ -405,7 +417,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
       it = c->graphs.emplace(key, exec).first;
     }
     JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
-    c->launches += 2 * (max_it + 1);
+    c->launches += (fused ? 1 : 2) * (max_it + 1);
     c->max_it_enqueued = max_it;
     return JOFC_OK;
   }
@@ -426,9 +438,11 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
       if (c->allreduce(exchange(c), fid_slot(c) + 1, c->stream, c->allreduce_user) != 0)
         return set_error(JOFC_ECOMM, "all-reduce hook failed at iteration %zu", t);
     }
-    rc = epi_for_d(c, ep);
-    if (rc) return rc;
-    ++c->launches;
+    if (!fused) {
+      rc = epi_for_d(c, ep);
+      if (rc) return rc;
+      ++c->launches;
+    }
   }
   if (events) JOFC_CUDA(cudaEventRecord((*events)[max_it + 1], c->stream));
   c->max_it_enqueued = max_it;
