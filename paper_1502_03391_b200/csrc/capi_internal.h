@@ -168,6 +168,8 @@ namespace capi {
 int copy_sync(jofc_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
 int prof_begin(jofc_ctx* c, cudaEvent_t* end);
 int require_problem(jofc_ctx* c);
+int diag_mode();
+long long fuse_epilogue_max_n();
 double band_cost();
 double block_cost(const Layout& L, int B, int J, bool enters_band);
 void make_layout(jofc_ctx* c, size_t m, size_t n);

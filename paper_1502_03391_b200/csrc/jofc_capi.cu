@@ -75,6 +75,24 @@ int require_problem(jofc_ctx* c) {
 // blocks (diagonal-crossing or padded) +0.1, the first block a CTA processes
 // of a row band +band_cost() (flush of the row sums, X row-block staging, two
 // CTA barriers; 1.0 measured best at C3/C4/C5 among 0, 0.5, 1, 1.5, 2, 4, 8).
+// Experiment switches, read once per process: JOFC_DIAG (pass-kernel timing
+// modes; results are wrong when set), JOFC_FUSE_EPI_N (fused-epilogue limit).
+int diag_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("JOFC_DIAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+long long fuse_epilogue_max_n() {
+  static const long long v = [] {
+    const char* e = std::getenv("JOFC_FUSE_EPI_N");
+    return e ? std::atoll(e) : kFuseEpilogueMaxN;
+  }();
+  return v;
+}
+
 double band_cost() {
   static const double v = [] {
     const char* e = std::getenv("JOFC_BAND_COST");  // experiments
@@ -337,10 +355,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   pp.end = L.end;
   pp.fid_slot = fid_slot(c);
   pp.bounds = c->bounds.p;
-  {
-    const char* dg = getenv("JOFC_DIAG");  // experiments only; results are wrong when set
-    pp.diag = dg ? atoi(dg) : 0;
-  }
+  pp.diag = diag_mode();
 
   EpiParams ep{};
   ep.x0 = c->x0.p;
@@ -359,11 +374,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   // Small problems on one GPU: the pass kernel's last CTA runs the epilogue
   // too (one launch per iteration instead of two).  The threshold keeps the
   // one-CTA epilogue below the cost of a second launch.
-  {
-    const char* e = std::getenv("JOFC_FUSE_EPI_N");  // experiments
-    const long long limit = e ? std::atoll(e) : kFuseEpilogueMaxN;
-    pp.fuse_epilogue = (c->world == 1 && L.n <= limit) ? 1 : 0;
-  }
+  pp.fuse_epilogue = (c->world == 1 && L.n <= fuse_epilogue_max_n()) ? 1 : 0;
   pp.epi = ep;
   const bool fused = pp.fuse_epilogue != 0;
 

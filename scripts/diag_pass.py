@@ -24,14 +24,24 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--n", type=int, default=None)
     a = ap.parse_args()
+    modes = [int(x) for x in a.modes.split(",")]
+    if len(modes) > 1 or os.environ.get("JOFC_DIAG", str(modes[0])) != str(modes[0]):
+        # the library reads JOFC_DIAG once per process: one process per mode
+        import subprocess
+        for mode in modes:
+            argv = [sys.executable, os.path.abspath(__file__), "--config", str(a.config),
+                    "--modes", str(mode), "--iters", str(a.iters)]
+            if a.n:
+                argv += ["--n", str(a.n)]
+            subprocess.run(argv, env=dict(os.environ, JOFC_DIAG=str(mode)), check=True)
+        return
     wl = workloads.make(a.config, n=a.n)
     dev = jg.Device(0)
     dev.upload_features(wl.in_features)
     x0 = wl.x0()
     lib = dev.lib
     pairs = dev.problem_pairs()
-    for mode in [int(x) for x in a.modes.split(",")]:
-        os.environ["JOFC_DIAG"] = str(mode)
+    for mode in modes:
         # single-pass solves (max_it = 0): every launch does the full pass even
         # when the experiment corrupts the iterate
         for rep in range(2):
@@ -44,7 +54,6 @@ def main():
         avg = ms.value / n.value
         print(f"cfg{a.config} mode {mode}: pass {avg:.4f} ms  {8 * pairs / avg / 1e6:.1f} GB/s "
               f"({n.value} launches)", flush=True)
-    os.environ.pop("JOFC_DIAG")
 
 
 if __name__ == "__main__":
