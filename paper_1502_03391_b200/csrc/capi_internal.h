@@ -22,6 +22,9 @@ namespace capi {
 
 // Largest n whose epilogue the pass kernel's last CTA runs itself (one GPU).
 constexpr long long kFuseEpilogueMaxN = 1024;
+// Synchronous solves stop enqueuing iterations once the device says done,
+// checked every kStopChunk iterations (at most ~2 chunks of no-op launches).
+constexpr size_t kStopChunk = 16;
 
 inline thread_local std::string g_error;
 
@@ -160,6 +163,10 @@ struct jofc_ctx {
   // host -> device upload: copies on their own stream, overlapped with packing
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t up_copied[2] = {nullptr, nullptr}, up_packed[2] = {nullptr, nullptr};
+  // early stop of synchronous solves: the done flag every kStopChunk
+  // iterations (pinned) and the events that say it has landed
+  int* stop_flag = nullptr;
+  cudaEvent_t stop_ev[2] = {nullptr, nullptr};
 };
 
 namespace jofc_gpu {

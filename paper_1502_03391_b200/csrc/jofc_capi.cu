@@ -305,7 +305,7 @@ int download_config(jofc_ctx* c, const double* src, double* x) {
 // evaluations) on the context stream.  events (optional) get max_it + 2
 // records: before pass t and after the final epilogue.
 int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x0, double eps,
-                  size_t max_it, std::vector<cudaEvent_t>* events) {
+                  size_t max_it, std::vector<cudaEvent_t>* events, bool early_stop = false) {
   int rc = require_problem(c);
   if (rc) return rc;
   if (d < 1 || d > static_cast<size_t>(kMaxD))
@@ -382,8 +382,31 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   // whole 2(max_it + 1)-kernel sequence (kernel parameters only hold buffer
   // pointers; everything iteration-dependent lives in the control block).
   const bool graphable = c->use_graphs && c->world == 1 && !events && !c->profiling;
+  if (early_stop && !c->stop_flag) {
+    JOFC_CUDA(cudaMallocHost(&c->stop_flag, 2 * sizeof(int)));
+    for (int k = 0; k < 2; ++k)
+      JOFC_CUDA(cudaEventCreateWithFlags(&c->stop_ev[k], cudaEventDisableTiming));
+  }
+  // early stop: after enqueuing chunk `ch` (0-based) of iterations, send its
+  // done flag to the host and look at the previous chunk's; true = stop
+  auto chunk_done = [&](size_t ch, bool* stop) -> int {
+    const int k = static_cast<int>(ch & 1);
+    JOFC_CUDA(cudaMemcpyAsync(&c->stop_flag[k], &c->ctrl.p->done, sizeof(int),
+                              cudaMemcpyDeviceToHost, c->stream));
+    JOFC_CUDA(cudaEventRecord(c->stop_ev[k], c->stream));
+    *stop = false;
+    if (ch >= 1) {
+      JOFC_CUDA(cudaEventSynchronize(c->stop_ev[k ^ 1]));
+      *stop = c->stop_flag[k ^ 1] != 0;
+    }
+    return JOFC_OK;
+  };
   if (graphable) {
-    std::vector<uintptr_t> key = {c->d, max_it, static_cast<uintptr_t>(c->pass_grid),
+    // one graph of the whole sequence, or (early stop) of one chunk replayed
+    // until the device says done: later iterations are no-ops on the device
+    // anyway (the control block), this stops paying their launches
+    const size_t per_graph = early_stop ? std::min(kStopChunk, max_it + 1) : max_it + 1;
+    std::vector<uintptr_t> key = {c->d, per_graph, static_cast<uintptr_t>(c->pass_grid),
                                   static_cast<uintptr_t>(c->epi_grid),
                                   reinterpret_cast<uintptr_t>(pp.delta),
                                   reinterpret_cast<uintptr_t>(pp.x0),
@@ -408,7 +431,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
       if (rc) return rc;
       JOFC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       int lrc = JOFC_OK;
-      for (size_t t = 0; t <= max_it && !lrc; ++t) {
+      for (size_t t = 0; t < per_graph && !lrc; ++t) {
         lrc = pass_for_d(c, pp);
         if (!lrc && !fused) lrc = epi_for_d(c, ep);
       }
@@ -427,13 +450,25 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
         return set_error(JOFC_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ie));
       it = c->graphs.emplace(key, exec).first;
     }
-    JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
-    c->launches += (fused ? 1 : 2) * (max_it + 1);
+    for (size_t ch = 0; ch * per_graph <= max_it; ++ch) {
+      JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
+      c->launches += (fused ? 1 : 2) * per_graph;
+      if (early_stop) {
+        bool stop = false;
+        JOFC_TRY(chunk_done(ch, &stop));
+        if (stop) break;
+      }
+    }
     c->max_it_enqueued = max_it;
     return JOFC_OK;
   }
 
   for (size_t t = 0; t <= max_it; ++t) {
+    if (early_stop && t > 0 && t % kStopChunk == 0) {
+      bool stop = false;
+      JOFC_TRY(chunk_done(t / kStopChunk - 1, &stop));
+      if (stop) break;
+    }
     if (events) JOFC_CUDA(cudaEventRecord((*events)[t], c->stream));
     cudaEvent_t pe1 = nullptr;
     rc = prof_begin(c, &pe1);
@@ -522,6 +557,9 @@ int jofc_ctx_destroy(jofc_ctx* c) {
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   if (c->ctrl_host) cudaFreeHost(c->ctrl_host);
   c->ingest.release();
+  if (c->stop_flag) cudaFreeHost(c->stop_flag);
+  for (auto& e : c->stop_ev)
+    if (e) cudaEventDestroy(e);
   for (int k = 0; k < 2; ++k) {
     if (c->up_copied[k]) cudaEventDestroy(c->up_copied[k]);
     if (c->up_packed[k]) cudaEventDestroy(c->up_packed[k]);
@@ -757,7 +795,8 @@ int jofc_fjofc_embed(jofc_ctx* c, const jofc_weights* spec, size_t d, const doub
     ev.resize(max_it + 2);
     for (auto& e : ev) JOFC_CUDA(cudaEventCreate(&e));
   }
-  int rc = enqueue_solve(c, spec, d, x0, eps, max_it, step_seconds ? &ev : nullptr);
+  int rc = enqueue_solve(c, spec, d, x0, eps, max_it, step_seconds ? &ev : nullptr,
+                         /*early_stop=*/true);
   size_t its = 0;
   if (!rc) rc = jofc_fetch_result(c, x_out, trace_out, &its, converged);
   if (!rc && iterations) *iterations = its;
