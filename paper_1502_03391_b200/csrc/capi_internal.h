@@ -24,7 +24,7 @@ namespace capi {
 constexpr long long kFuseEpilogueMaxN = 1024;
 // Synchronous solves stop enqueuing iterations once the device says done,
 // checked every kStopChunk iterations (at most ~2 chunks of no-op launches).
-constexpr size_t kStopChunk = 16;
+constexpr size_t kStopChunk = 32;
 
 inline thread_local std::string g_error;
 
@@ -176,6 +176,7 @@ int copy_sync(jofc_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyK
 int prof_begin(jofc_ctx* c, cudaEvent_t* end);
 int require_problem(jofc_ctx* c);
 int diag_mode();
+size_t stop_chunk();
 long long fuse_epilogue_max_n();
 double band_cost();
 double block_cost(const Layout& L, int B, int J, bool enters_band);

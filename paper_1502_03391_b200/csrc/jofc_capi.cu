@@ -93,6 +93,16 @@ long long fuse_epilogue_max_n() {
   return v;
 }
 
+// Chunk length of the synchronous solves' early stop (0: off); JOFC_STOP_CHUNK
+// overrides kStopChunk (experiments).
+size_t stop_chunk() {
+  static const size_t v = [] {
+    const char* e = std::getenv("JOFC_STOP_CHUNK");
+    return e ? static_cast<size_t>(std::atoll(e)) : kStopChunk;
+  }();
+  return v;
+}
+
 double band_cost() {
   static const double v = [] {
     const char* e = std::getenv("JOFC_BAND_COST");  // experiments
@@ -405,7 +415,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
     // one graph of the whole sequence, or (early stop) of one chunk replayed
     // until the device says done: later iterations are no-ops on the device
     // anyway (the control block), this stops paying their launches
-    const size_t per_graph = early_stop ? std::min(kStopChunk, max_it + 1) : max_it + 1;
+    const size_t per_graph = early_stop ? std::min(stop_chunk(), max_it + 1) : max_it + 1;
     std::vector<uintptr_t> key = {c->d, per_graph, static_cast<uintptr_t>(c->pass_grid),
                                   static_cast<uintptr_t>(c->epi_grid),
                                   reinterpret_cast<uintptr_t>(pp.delta),
@@ -464,9 +474,9 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   }
 
   for (size_t t = 0; t <= max_it; ++t) {
-    if (early_stop && t > 0 && t % kStopChunk == 0) {
+    if (early_stop && t > 0 && t % stop_chunk() == 0) {
       bool stop = false;
-      JOFC_TRY(chunk_done(t / kStopChunk - 1, &stop));
+      JOFC_TRY(chunk_done(t / stop_chunk() - 1, &stop));
       if (stop) break;
     }
     if (events) JOFC_CUDA(cudaEventRecord((*events)[t], c->stream));
@@ -796,7 +806,7 @@ int jofc_fjofc_embed(jofc_ctx* c, const jofc_weights* spec, size_t d, const doub
     for (auto& e : ev) JOFC_CUDA(cudaEventCreate(&e));
   }
   int rc = enqueue_solve(c, spec, d, x0, eps, max_it, step_seconds ? &ev : nullptr,
-                         /*early_stop=*/true);
+                         /*early_stop=*/stop_chunk() > 0);
   size_t its = 0;
   if (!rc) rc = jofc_fetch_result(c, x_out, trace_out, &its, converged);
   if (!rc && iterations) *iterations = its;
