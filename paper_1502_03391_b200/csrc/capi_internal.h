@@ -158,6 +158,7 @@ struct jofc_ctx {
   // oos state
   DevBuf<double> oos_x, oos_delta, oos_y0, oos_y1, oos_part, oos_trace;
   DevBuf<OosPoint> oos_st;
+  DevBuf<unsigned> oos_done;
   // streaming ingest staging
   IngestPanels ingest;
   // host -> device upload: copies on their own stream, overlapped with packing

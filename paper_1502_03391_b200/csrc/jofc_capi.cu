@@ -868,11 +868,20 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
   const dim3 pg((op.k + kOosWarps - 1) / kOosWarps, op.m,
                 static_cast<unsigned>(std::min<long long>(kOosSplits, std::max<long long>(1, op.n / 256))));
   const unsigned ug = (op.k + 127) / 128;
-  // The 2(steps + 1) launches are replayed from a captured CUDA graph (all
-  // per-step state is in the device-side point records).
+  // The launches are replayed from a captured CUDA graph of `per_graph` steps
+  // (all per-step state is in the device-side point records), chunk after
+  // chunk until every point is done: the count of finished points is read one
+  // chunk behind, so at most ~2 chunks of no-op launches follow the last point.
+  const size_t chunk = stop_chunk() ? stop_chunk() : static_cast<size_t>(steps) + 1;
+  const size_t per_graph = std::min(chunk, static_cast<size_t>(steps) + 1);
+  if (!c->stop_flag) {
+    JOFC_CUDA(cudaMallocHost(&c->stop_flag, 2 * sizeof(int)));
+    for (int k = 0; k < 2; ++k)
+      JOFC_CUDA(cudaEventCreateWithFlags(&c->stop_ev[k], cudaEventDisableTiming));
+  }
   std::vector<uintptr_t> key = {0x0005u, static_cast<uintptr_t>(D), static_cast<uintptr_t>(op.k),
                                 static_cast<uintptr_t>(op.m), static_cast<uintptr_t>(op.n),
-                                static_cast<uintptr_t>(steps), static_cast<uintptr_t>(op.fixed),
+                                static_cast<uintptr_t>(per_graph), static_cast<uintptr_t>(op.fixed),
                                 static_cast<uintptr_t>(op.max_it),
                                 reinterpret_cast<uintptr_t>(op.x),
                                 reinterpret_cast<uintptr_t>(op.deltas),
@@ -880,7 +889,8 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
                                 reinterpret_cast<uintptr_t>(op.y1),
                                 reinterpret_cast<uintptr_t>(op.part),
                                 reinterpret_cast<uintptr_t>(op.st),
-                                reinterpret_cast<uintptr_t>(op.traces)};
+                                reinterpret_cast<uintptr_t>(op.traces),
+                                reinterpret_cast<uintptr_t>(op.done_count)};
   uint64_t wbits, ebits;
   std::memcpy(&wbits, &op.w, 8);
   std::memcpy(&ebits, &op.eps, 8);
@@ -897,7 +907,7 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
     if (smem > 48 * 1024)
       JOFC_CUDA(cudaFuncSetAttribute(jofc_oos_pass_kernel<D>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    for (int t = 0; t <= steps; ++t) {
+    for (size_t t = 0; t < per_graph; ++t) {
       jofc_oos_pass_kernel<D><<<pg, kOosWarps * 32, smem, c->stream>>>(op);
       jofc_oos_update_kernel<D><<<ug, 128, 0, c->stream>>>(op);
     }
@@ -912,8 +922,18 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
       return set_error(JOFC_ECUDA, "oos graph instantiate failed: %s", cudaGetErrorString(ie));
     it = c->graphs.emplace(key, exec).first;
   }
-  JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
-  c->launches += 2 * (steps + 1);
+  for (size_t ch = 0; ch * per_graph <= static_cast<size_t>(steps); ++ch) {
+    JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
+    c->launches += 2 * per_graph;
+    const int kk = static_cast<int>(ch & 1);
+    JOFC_CUDA(cudaMemcpyAsync(&c->stop_flag[kk], op.done_count, sizeof(unsigned),
+                              cudaMemcpyDeviceToHost, c->stream));
+    JOFC_CUDA(cudaEventRecord(c->stop_ev[kk], c->stream));
+    if (ch >= 1) {
+      JOFC_CUDA(cudaEventSynchronize(c->stop_ev[kk ^ 1]));
+      if (static_cast<unsigned>(c->stop_flag[kk ^ 1]) >= static_cast<unsigned>(op.k)) break;
+    }
+  }
   return JOFC_OK;
 }
 
@@ -934,6 +954,8 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
   JOFC_CUDA(c->oos_part.ensure(k * m * (d + 2) + k));
   JOFC_CUDA(c->oos_trace.ensure(k * (max_it + 1)));
   JOFC_CUDA(c->oos_st.ensure(k));
+  JOFC_CUDA(c->oos_done.ensure(1));
+  JOFC_CUDA(cudaMemsetAsync(c->oos_done.p, 0, sizeof(unsigned), c->stream));
   JOFC_CUDA(cudaMemcpyAsync(c->oos_x.p, x, m * n * d * sizeof(double), cudaMemcpyDefault, c->stream));
   JOFC_CUDA(cudaMemcpyAsync(c->oos_delta.p, deltas, k * m * n * sizeof(double), cudaMemcpyDefault,
                             c->stream));
@@ -948,6 +970,7 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
   op.y1 = c->oos_y1.p;
   op.part = c->oos_part.p;
   op.st = c->oos_st.p;
+  op.done_count = c->oos_done.p;
   op.traces = c->oos_trace.p;
   op.k = static_cast<int>(k);
   op.m = static_cast<int>(m);

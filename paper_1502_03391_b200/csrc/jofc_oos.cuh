@@ -43,6 +43,7 @@ struct OosParams {
   double w, eps, term_count;
   int max_it;
   int fixed;
+  unsigned* done_count;  // points finished (the host stops enqueuing at k)
 };
 
 constexpr int kOosWarps = 8;
@@ -205,12 +206,14 @@ __global__ void __launch_bounds__(128) jofc_oos_update_kernel(const OosParams p)
     st.done = 1;
     st.iterations = t;
     p.st[pt] = st;
+    atomicAdd(p.done_count, 1u);
     return;
   }
   st.iterations = t;
   double* prev_slot = p.part + static_cast<long long>(p.k) * m * (D + 2) + pt;
   if (t >= 1 && !p.fixed && (*prev_slot - sigma) / p.term_count < p.eps) st.done = 1;
   if (t >= p.max_it) st.done = 1;
+  if (st.done) atomicAdd(p.done_count, 1u);
   *prev_slot = sigma;
   if (!st.done) {
     const double nn = static_cast<double>(p.n);

@@ -20,3 +20,16 @@ for cfg, n in ((1, None), (5, 2000)):
     dt = time.perf_counter() - t0
     print(f"cfg{cfg} n={wl.n}: {r.iterations} iterations ({r.terminated.name}), "
           f"{dt * 1e3:.2f} ms, launches {dev.launches()}")
+
+# one out-of-sample point with the default options (eps 1e-6, 1000 iterations)
+import numpy as np  # noqa: E402
+
+wl = workloads.make(5, n=2000)
+x = np.random.default_rng(0).normal(size=(wl.m, wl.n, wl.d))
+od = np.abs(np.random.default_rng(1).normal(size=(wl.m, wl.n))) + 1.0
+dev = jg.Device(0)
+jg.oos_embed(x, od, 0.5, jg.OosOptions(), 7, device=dev)
+t0 = time.perf_counter()
+res = jg.oos_embed(x, od, 0.5, jg.OosOptions(), 7, device=dev)
+print(f"oos_embed n={wl.n}: {res.iterations} iterations ({res.terminated.name}), "
+      f"{(time.perf_counter() - t0) * 1e3:.2f} ms, launches {dev.launches()}")
