@@ -872,7 +872,9 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
   // (all per-step state is in the device-side point records), chunk after
   // chunk until every point is done: the count of finished points is read one
   // chunk behind, so at most ~2 chunks of no-op launches follow the last point.
-  const size_t chunk = stop_chunk() ? stop_chunk() : static_cast<size_t>(steps) + 1;
+  // (fixed iteration counts cannot stop early: one graph of all steps)
+  const size_t chunk =
+      (stop_chunk() && !op.fixed) ? stop_chunk() : static_cast<size_t>(steps) + 1;
   const size_t per_graph = std::min(chunk, static_cast<size_t>(steps) + 1);
   if (!c->stop_flag) {
     JOFC_CUDA(cudaMallocHost(&c->stop_flag, 2 * sizeof(int)));
