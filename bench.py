@@ -181,7 +181,12 @@ def run_ours(args):
     dev.upload_features(wl.in_features)
     x0_host = wl.x0()
     x0_dev = torch.from_numpy(x0_host).cuda()
-    if world > 1:
+    if world > 1 and args.exchange == "peer":
+        # products and configuration rows through peer memory inside the
+        # loop's own kernels (csrc/jofc_peer.cuh), slabs mapped by CUDA IPC
+        from paper_1502_03391_b200.dist import attach_peers
+        attach_peers(dev)
+    elif world > 1:
         from paper_1502_03391_b200.dist import attach_nccl
         attach_nccl(dev, wl.d)  # torch-owned exchange buffer, NCCL all-reduce on dev.stream
 
@@ -299,8 +304,11 @@ def run_ours(args):
                        "launch": "CUDA graph replay" if args.graphs else "stream launches",
                        "delta_bytes_resident_per_gpu": local_bytes,
                        "parallelism": f"delta-shard{world}" if world > 1 else "single",
-                       "collective": (f"{backend} all-reduce of P + fidelity per iteration"
-                                      if world > 1 else None),
+                       "collective": (None if world == 1 else
+                                      "peer memory: reduce-scatter read + mix + all-gather "
+                                      "write in the loop's kernels (NVLink loads/stores)"
+                                      if args.exchange == "peer" else
+                                      f"{backend} all-reduce of P + fidelity per iteration"),
                        "l2": "inputs larger than L2 (packed Delta %.2f GB vs 126 MB L2)" % (local_bytes / 1e9)
                        if local_bytes > 126e6 * 4 else "Delta may be L2-resident"},
             "delta_entries_per_s": value * pairs,
@@ -820,6 +828,9 @@ def main():
                     help="averaged_procrustes_init on the resident Delta (SURVEY 8f row f1)")
     ap.add_argument("--ingest", action="store_true",
                     help="stream a .jofc problem file into the device layout (SURVEY 8f row f2)")
+    ap.add_argument("--exchange", default=os.environ.get("JOFC_EXCHANGE", "nccl"),
+                    choices=["nccl", "peer"],
+                    help="multi-GPU exchange: NCCL all-reduce hook or peer-memory kernels")
     ap.add_argument("--graphs", type=int, default=None,
                     help="replay CUDA graphs in the timed region (default: on for configs 1,2,5)")
     args = ap.parse_args()

@@ -137,6 +137,31 @@ int jofc_profile_read(jofc_ctx* ctx, double* pass_ms, uint64_t* pass_launches);
 int jofc_set_exchange_buffer(jofc_ctx* ctx, double* device_buf, size_t capacity);
 size_t jofc_exchange_count(jofc_ctx* ctx, size_t d);
 
+/* Peer-memory exchange (NVLink / NVSwitch), the alternative to the all-reduce
+ * hook: the exchange of the products (the hook's all-reduce + epilogue) becomes
+ * two kernels that read the world's partial products and write the mixed
+ * configuration straight through peer pointers
+ * (paper_1502_03391_b200/csrc/jofc_peer.cuh).
+ * Same SPMD call sequence on every rank, after jofc_set_shard and the problem:
+ *   jofc_peer_export(ctx, handle, NULL)     64-byte CUDA IPC handle of this
+ *                                           rank's exchange slab
+ *   (the caller all-gathers the handles, rank order)
+ *   jofc_peer_attach(ctx, rank, world, handles)   handles: world x 64 bytes
+ * then the usual solve / stress / step calls; every rank must make the same
+ * calls in the same order.  world <= 16.  jofc_peer_attach_pointers takes
+ * device pointers of slabs instead of IPC handles (contexts of one process);
+ * jofc_peer_detach reverts to the hook.  Re-export after a new problem. */
+int jofc_peer_export(jofc_ctx* ctx, void* ipc_handle_out, void** slab_out);
+int jofc_peer_attach(jofc_ctx* ctx, int rank, int world, const void* handles);
+int jofc_peer_attach_pointers(jofc_ctx* ctx, int rank, int world, void* const* slabs);
+int jofc_peer_detach(jofc_ctx* ctx);
+/* Test driver: one solve over `world` peer-attached contexts of ONE process,
+ * launched stage by stage with stream-event ordering so that no kernel ever
+ * waits for a flag another context has not raised yet (a single GPU can host
+ * all ranks).  Results via jofc_fetch_result on each context. */
+int jofc_peer_lockstep_solve(jofc_ctx* const* ctxs, int world, const jofc_weights* spec, size_t d,
+                             const double* x0, double eps, size_t max_iterations);
+
 /* Out-of-sample (proj/src/oos.cpp), uniform w only as in the reference.
  * x: frozen configuration m x n x d; deltas: m x n for one point. */
 int jofc_oos_stress(jofc_ctx* ctx, size_t m, size_t n, size_t d, const double* y,

@@ -27,6 +27,7 @@ from .api import (  # noqa: F401
     oos_start,
     oos_step_fast,
     oos_stress,
+    peer_lockstep_solve,
     raw_stress,
     stress_pair_count,
     symmetric_top_eigenpairs_subspace,

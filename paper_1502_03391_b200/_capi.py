@@ -82,6 +82,12 @@ _SIGS = {
     "jofc_profile_read": (C.c_int, [_vp, _dp, C.POINTER(C.c_uint64)]),
     "jofc_set_exchange_buffer": (C.c_int, [_vp, _vp, _sz]),
     "jofc_exchange_count": (_sz, [_vp, _sz]),
+    "jofc_peer_export": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
+    "jofc_peer_attach": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
+    "jofc_peer_attach_pointers": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "jofc_peer_detach": (C.c_int, [_vp]),
+    "jofc_peer_lockstep_solve": (C.c_int, [C.POINTER(_vp), C.c_int, C.POINTER(Weights), _sz, _dp,
+                                           C.c_double, _sz]),
     "jofc_oos_stress": (C.c_int, [_vp, _sz, _sz, _sz, _dp, _dp, _dp, C.c_double, _dp]),
     "jofc_oos_step": (C.c_int, [_vp, _sz, _sz, _sz, _dp, _dp, _dp, C.c_double, _dp]),
     "jofc_oos_batch": (C.c_int, [_vp, _sz, _sz, _sz, _sz, _dp, _dp, C.c_double, _dp, C.c_double,

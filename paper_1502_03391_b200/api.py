@@ -289,6 +289,30 @@ class Device:
         self._hook = _capi.ALLREDUCE_FN(tramp)
         check(self.lib.jofc_set_allreduce(self.h, self._hook, None))
 
+    # peer-memory exchange (include/jofc_gpu.h, jofc_peer_*): multi-GPU
+    # without the all-reduce hook; paper_1502_03391_b200.dist.attach_peers
+    # runs the SPMD export / all-gather / attach sequence
+    def peer_export(self):
+        """(64-byte CUDA IPC handle, device pointer) of this rank's slab."""
+        buf = C.create_string_buffer(64)
+        slab = C.c_void_p()
+        check(self.lib.jofc_peer_export(self.h, buf, C.byref(slab)))
+        return buf.raw, slab.value
+
+    def peer_attach(self, rank, world, handles):
+        """handles: the world's 64-byte handles, rank order."""
+        blob = b"".join(handles)
+        if len(blob) != 64 * world:
+            raise InvalidArgument("peer exchange: need world x 64-byte handles")
+        check(self.lib.jofc_peer_attach(self.h, int(rank), int(world), blob))
+
+    def peer_attach_pointers(self, rank, world, slabs):
+        arr = (C.c_void_p * world)(*slabs)
+        check(self.lib.jofc_peer_attach_pointers(self.h, int(rank), int(world), arr))
+
+    def peer_detach(self):
+        check(self.lib.jofc_peer_detach(self.h))
+
     def load_files(self, paths, normalize=False):
         enc = [os.fsencode(p) for p in paths]
         arr = (C.c_char_p * len(enc))(*enc)
@@ -465,6 +489,27 @@ def fjofc_embed(problem, spec, options: SolveOptions, device=None):
                            terminated=Termination.converged if conv.value else
                            Termination.max_iterations,
                            step_seconds=steps[:k].tolist())
+
+
+def peer_lockstep_solve(devices, spec, x0, eps, max_iterations):
+    """One fJOFC solve over peer-attached contexts of this process (test
+    driver of the peer exchange: jofc_peer_lockstep_solve).  Returns, per
+    rank, (X, stress trace, iterations, converged)."""
+    x0 = _f64(x0)
+    m, n, d = x0.shape
+    world = len(devices)
+    arr = (C.c_void_p * world)(*[dv.h.value for dv in devices])
+    lib = devices[0].lib
+    check(lib.jofc_peer_lockstep_solve(arr, world, C.byref(spec.c()), d, dptr(x0), float(eps),
+                                       int(max_iterations)))
+    out = []
+    for dv in devices:
+        x = np.empty_like(x0)
+        trace = np.empty(int(max_iterations) + 1)
+        its, conv = C.c_size_t(), C.c_int()
+        check(lib.jofc_fetch_result(dv.h, dptr(x), dptr(trace), C.byref(its), C.byref(conv)))
+        out.append((x, trace[: its.value + 1].copy(), its.value, bool(conv.value)))
+    return out
 
 
 def _embed_with_config_trace(problem, spec, options, x0, dev):

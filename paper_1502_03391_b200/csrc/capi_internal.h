@@ -16,6 +16,7 @@
 #include "jofc_gpu.h"
 #include "jofc_kernels.cuh"
 #include "jofc_oos.cuh"
+#include "jofc_peer.cuh"
 
 namespace jofc_gpu {
 namespace capi {
@@ -53,6 +54,23 @@ inline int set_error(int code, const char* fmt, ...) {
   } while (0)
 
 constexpr int kMaxD = 10;
+
+// FN<D>(args) for the runtime dimension d (1..kMaxD)
+#define JOFC_DISPATCH_D(d, FN, ...)         \
+  switch (d) {                              \
+    case 1: return FN<1>(__VA_ARGS__);      \
+    case 2: return FN<2>(__VA_ARGS__);      \
+    case 3: return FN<3>(__VA_ARGS__);      \
+    case 4: return FN<4>(__VA_ARGS__);      \
+    case 5: return FN<5>(__VA_ARGS__);      \
+    case 6: return FN<6>(__VA_ARGS__);      \
+    case 7: return FN<7>(__VA_ARGS__);      \
+    case 8: return FN<8>(__VA_ARGS__);      \
+    case 9: return FN<9>(__VA_ARGS__);      \
+    case 10: return FN<10>(__VA_ARGS__);    \
+    default:                                \
+      return set_error(JOFC_EINVAL, "dim %zu unsupported (1..10)", static_cast<size_t>(d)); \
+  }
 
 template <class T>
 struct DevBuf {
@@ -112,6 +130,25 @@ struct IngestPanels {
   }
 };
 
+// Peer-memory exchange state of a sharded context (capi_peer.cu).
+struct PeerState {
+  bool active = false;
+  int rank = 0, world = 1;
+  double* slab = nullptr;  // own slab (cudaMalloc: IPC-exportable)
+  size_t slab_doubles = 0;
+  long long p_off[2] = {0, 0}, x_off[2] = {0, 0};
+  long long p_len = 0, com_off = 0, flag1_off = 0, flag2_off = 0;
+  std::vector<long long> key;   // (m, n_pad) the slab is laid out for
+  std::vector<void*> opened;    // IPC-mapped peer slabs
+  DevBuf<double*> ptrs;         // device array of the world's slab bases
+  DevBuf<double> com_part;      // per mix CTA
+  unsigned epoch = 0;           // solves started (flags carry it)
+  int phase = 0;                // P region of the next solve's iteration 0
+  bool pending = false;         // a solve was enqueued and not yet finished
+  long long row_lo = 0, row_hi = 0;
+  int rows_cta = 32, mix_grid = 1;
+};
+
 }  // namespace capi
 }  // namespace jofc_gpu
 
@@ -168,6 +205,8 @@ struct jofc_ctx {
   // iterations (pinned) and the events that say it has landed
   int* stop_flag = nullptr;
   cudaEvent_t stop_ev[2] = {nullptr, nullptr};
+  // peer-memory exchange (multi-GPU without NCCL)
+  jofc_gpu::capi::PeerState peer;
 };
 
 namespace jofc_gpu {
@@ -182,6 +221,19 @@ long long fuse_epilogue_max_n();
 double band_cost();
 double block_cost(const Layout& L, int B, int J, bool enters_band);
 void make_layout(jofc_ctx* c, size_t m, size_t n);
+int finish_solve(jofc_ctx* c, Control* out);
+// configuration buffer k (0/1): the context's own, or its peer slab's
+double* xbuf(jofc_ctx* c, int k);
+// launches of the D-templated kernels (c->d)
+int pass_for_d(jofc_ctx* c, const PassParams& pp);
+// everything before the first launch of a solve (validation, weights,
+// buffers, X0, control block); fills the kernel parameters
+int prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x0, double eps,
+                  size_t max_it, PassParams* pp, EpiParams* ep);
+// peer exchange: stage 0 pass, 1 mix, 2 decide of iteration t
+int peer_stage(jofc_ctx* c, const PassParams& pp, size_t t, int stage);
+int peer_check(jofc_ctx* c);
+void peer_release(jofc_ctx* c);
 
 }  // namespace capi
 }  // namespace jofc_gpu

@@ -166,6 +166,15 @@ double* exchange(jofc_ctx* c) {
   return (c->ext_P && c->ext_cap >= need) ? c->ext_P : c->P.p;
 }
 
+}  // namespace
+
+double* jofc_gpu::capi::xbuf(jofc_ctx* c, int k) {
+  if (c->peer.active) return c->peer.slab + c->peer.x_off[k];
+  return k ? c->x1.p : c->x0.p;
+}
+
+namespace {
+
 size_t fid_slot(const jofc_ctx* c) { return static_cast<size_t>(c->lay.m) * c->lay.n_pad * c->d; }
 
 template <int D>
@@ -200,25 +209,17 @@ int launch_epi(jofc_ctx* c, const EpiParams& ep) {
   return JOFC_OK;
 }
 
-#define JOFC_DISPATCH_D(d, FN, ...)         \
-  switch (d) {                              \
-    case 1: return FN<1>(__VA_ARGS__);      \
-    case 2: return FN<2>(__VA_ARGS__);      \
-    case 3: return FN<3>(__VA_ARGS__);      \
-    case 4: return FN<4>(__VA_ARGS__);      \
-    case 5: return FN<5>(__VA_ARGS__);      \
-    case 6: return FN<6>(__VA_ARGS__);      \
-    case 7: return FN<7>(__VA_ARGS__);      \
-    case 8: return FN<8>(__VA_ARGS__);      \
-    case 9: return FN<9>(__VA_ARGS__);      \
-    case 10: return FN<10>(__VA_ARGS__);    \
-    default:                                \
-      return set_error(JOFC_EINVAL, "dim %zu unsupported (1..10)", static_cast<size_t>(d)); \
-  }
 
 
 
-int pass_for_d(jofc_ctx* c, const PassParams& pp) { JOFC_DISPATCH_D(c->d, launch_pass, c, pp); }
+}  // namespace
+
+int jofc_gpu::capi::pass_for_d(jofc_ctx* c, const PassParams& pp) {
+  JOFC_DISPATCH_D(c->d, launch_pass, c, pp);
+}
+
+namespace {
+
 int setup_for_d(jofc_ctx* c) { JOFC_DISPATCH_D(c->d, setup_for, c); }
 int epi_for_d(jofc_ctx* c, const EpiParams& ep) { JOFC_DISPATCH_D(c->d, launch_epi, c, ep); }
 
@@ -267,14 +268,17 @@ int pass_bounds(jofc_ctx* c) {
 int alloc_solve_state(jofc_ctx* c, size_t d, size_t max_it) {
   const Layout& L = c->lay;
   const size_t cfg = static_cast<size_t>(L.m) * L.n_pad * d;
-  const bool resize = (d != c->d) || !c->x0.p || c->x0.n < cfg;
+  const bool peer = c->peer.active;
+  const bool resize = !peer && ((d != c->d) || !c->x0.p || c->x0.n < cfg);
   c->d = d;
-  JOFC_CUDA(c->x0.ensure(cfg));
-  JOFC_CUDA(c->x1.ensure(cfg));
-  if (c->ext_P && c->ext_cap >= cfg + 1) {
-    c->P.release();
-  } else {
-    JOFC_CUDA(c->P.ensure(cfg + 1));
+  if (!peer) {  // (peer exchange: X and P live in the context's slab)
+    JOFC_CUDA(c->x0.ensure(cfg));
+    JOFC_CUDA(c->x1.ensure(cfg));
+    if (c->ext_P && c->ext_cap >= cfg + 1) {
+      c->P.release();
+    } else {
+      JOFC_CUDA(c->P.ensure(cfg + 1));
+    }
   }
   c->pass_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(c->num_sms, L.local())));
   c->epi_grid = static_cast<int>((L.n + 255) / 256);
@@ -288,7 +292,8 @@ int alloc_solve_state(jofc_ctx* c, size_t d, size_t max_it) {
     JOFC_CUDA(cudaMemsetAsync(c->x0.p, 0, cfg * sizeof(double), c->stream));
     JOFC_CUDA(cudaMemsetAsync(c->x1.p, 0, cfg * sizeof(double), c->stream));
   }
-  JOFC_CUDA(cudaMemsetAsync(exchange(c), 0, (cfg + 1) * sizeof(double), c->stream));
+  // (peer exchange: the protocol leaves the next solve's P region zeroed)
+  if (!peer) JOFC_CUDA(cudaMemsetAsync(exchange(c), 0, (cfg + 1) * sizeof(double), c->stream));
   return JOFC_OK;
 }
 
@@ -314,8 +319,11 @@ int download_config(jofc_ctx* c, const double* src, double* x) {
 // Enqueue the whole majorization (max_it transforms, max_it + 1 stress
 // evaluations) on the context stream.  events (optional) get max_it + 2
 // records: before pass t and after the final epilogue.
-int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x0, double eps,
-                  size_t max_it, std::vector<cudaEvent_t>* events, bool early_stop = false) {
+}  // namespace
+
+int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t d,
+                                  const double* x0, double eps, size_t max_it, PassParams* ppo,
+                                  EpiParams* epo) {
   int rc = require_problem(c);
   if (rc) return rc;
   if (d < 1 || d > static_cast<size_t>(kMaxD))
@@ -327,6 +335,13 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   std::string msg;
   rc = build_weights(spec, static_cast<size_t>(L.m), static_cast<size_t>(L.n), &hw, &msg);
   if (rc) return set_error(rc, "%s", msg.c_str());
+  if (c->peer.active) {
+    if (c->peer.pending) {  // the previous solve fixes this one's P parity
+      Control prev;
+      finish_solve(c, &prev);
+    }
+    JOFC_TRY(peer_check(c));
+  }
   rc = alloc_solve_state(c, d, max_it);
   if (rc) return rc;
 
@@ -338,21 +353,25 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   std::copy(hw.within.begin(), hw.within.end(), consts.begin() + 3 * mm);
   JOFC_CUDA(cudaMemcpyAsync(c->consts.p, consts.data(), consts.size() * sizeof(double),
                             cudaMemcpyHostToDevice, c->stream));
-  rc = upload_config(c, x0, c->x0.p);
+  rc = upload_config(c, x0, xbuf(c, 0));
   if (rc) return rc;
 
   Control& h = *c->ctrl_host;
   std::memset(&h, 0, sizeof(Control));
   h.max_it = static_cast<int>(max_it);
   h.eps = eps;
+  if (c->peer.active) {
+    h.epoch = ++c->peer.epoch;
+    c->peer.pending = true;
+  }
   const double mn = static_cast<double>(L.m) * static_cast<double>(L.n);
   h.pairs = mn * (mn - 1.0) / 2.0;
   JOFC_CUDA(cudaMemcpyAsync(c->ctrl.p, &h, sizeof(Control), cudaMemcpyHostToDevice, c->stream));
 
   PassParams pp{};
   pp.delta = c->delta.p;
-  pp.x0 = c->x0.p;
-  pp.x1 = c->x1.p;
+  pp.x0 = xbuf(c, 0);
+  pp.x1 = xbuf(c, 1);
   pp.P = exchange(c);
   pp.fid_partials = c->fid_part.p;
   pp.ctrl = c->ctrl.p;
@@ -368,8 +387,8 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   pp.diag = diag_mode();
 
   EpiParams ep{};
-  ep.x0 = c->x0.p;
-  ep.x1 = c->x1.p;
+  ep.x0 = xbuf(c, 0);
+  ep.x1 = xbuf(c, 1);
   ep.P = exchange(c);
   ep.com_partials = c->com_part.p;
   ep.trace = c->trace.p;
@@ -386,6 +405,20 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   // one-CTA epilogue below the cost of a second launch.
   pp.fuse_epilogue = (c->world == 1 && L.n <= fuse_epilogue_max_n()) ? 1 : 0;
   pp.epi = ep;
+  *ppo = pp;
+  *epo = ep;
+  return JOFC_OK;
+}
+
+namespace {
+
+int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x0, double eps,
+                  size_t max_it, std::vector<cudaEvent_t>* events, bool early_stop = false) {
+  PassParams pp;
+  EpiParams ep;
+  int rc = prepare_solve(c, spec, d, x0, eps, max_it, &pp, &ep);
+  if (rc) return rc;
+  const Layout& L = c->lay;
   const bool fused = pp.fuse_epilogue != 0;
 
   // Single GPU, no per-launch events: replay a captured CUDA graph of the
@@ -483,6 +516,13 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
     cudaEvent_t pe1 = nullptr;
     rc = prof_begin(c, &pe1);
     if (rc) return rc;
+    if (c->peer.active) {  // pass + peer mix + decide (jofc_peer.cuh)
+      for (int stage = 0; stage < 3; ++stage) {
+        JOFC_TRY(peer_stage(c, pp, t, stage));
+        if (stage == 0 && pe1) JOFC_CUDA(cudaEventRecord(pe1, c->stream));
+      }
+      continue;
+    }
     rc = pass_for_d(c, pp);
     if (rc) return rc;
     if (pe1) JOFC_CUDA(cudaEventRecord(pe1, c->stream));
@@ -505,12 +545,21 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   return JOFC_OK;
 }
 
+}  // namespace
+
 // Synchronise, then fetch the control block; maps device status to errors.
-int finish_solve(jofc_ctx* c, Control* out) {
+int jofc_gpu::capi::finish_solve(jofc_ctx* c, Control* out) {
   JOFC_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl.p, sizeof(Control), cudaMemcpyDeviceToHost,
                             c->stream));
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
   *out = *c->ctrl_host;
+  if (c->peer.active && c->peer.pending) {
+    // the last evaluated iteration T left P region (T + phase) & 1 dirty and
+    // zeroed the other one: the next solve starts on the clean region
+    const int last = (out->status == 2) ? out->err_iter : out->iterations;
+    c->peer.phase = (c->peer.phase + last + 1) & 1;
+    c->peer.pending = false;
+  }
   if (out->status == 2) {
     if (out->err_iter == 0)
       return set_error(JOFC_ENUMERIC, "embed: non-finite stress at the initial configuration");
@@ -519,8 +568,6 @@ int finish_solve(jofc_ctx* c, Control* out) {
   if (!out->done) return set_error(JOFC_ECUDA, "solve did not terminate (internal)");
   return JOFC_OK;
 }
-
-}  // namespace
 
 // ======================================================================= C ABI
 extern "C" {
@@ -554,6 +601,7 @@ int jofc_ctx_destroy(jofc_ctx* c) {
   if (!c) return JOFC_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  peer_release(c);
   for (DevBuf<double>* b : {&c->delta, &c->x0, &c->x1, &c->P, &c->fid_part, &c->com_part,
                             &c->trace, &c->consts, &c->oos_x, &c->oos_delta, &c->oos_y0,
                             &c->oos_y1, &c->oos_part, &c->oos_trace})
@@ -783,7 +831,7 @@ int jofc_fetch_result(jofc_ctx* c, double* x_out, double* trace_out, size_t* ite
   rc = finish_solve(c, &h);
   if (rc) return rc;
   if (x_out) {
-    rc = download_config(c, (h.iterations & 1) ? c->x1.p : c->x0.p, x_out);
+    rc = download_config(c, xbuf(c, h.iterations & 1), x_out);
     if (rc) return rc;
   }
   if (trace_out)
@@ -851,7 +899,7 @@ int jofc_guttman_step(jofc_ctx* c, const jofc_weights* spec, size_t d, const dou
   // enqueue_solve(max_it = 0) marks the solve done at t = 0 after the mix, so
   // buffer 1 holds the transform of x.
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
-  rc = download_config(c, c->x1.p, x_next);
+  rc = download_config(c, xbuf(c, 1), x_next);
   if (rc) return rc;
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
   return JOFC_OK;

@@ -1,5 +1,9 @@
 """Multi-GPU plumbing for the sharded Guttman loop (one process per GPU).
 
+Two exchanges: attach_nccl (the all-reduce hook below) and attach_peers (the
+products and configuration rows move through peer memory inside the loop's
+own kernels, csrc/jofc_peer.cuh).
+
 Each rank owns a balanced contiguous range of the packed Delta block stream
 (jofc_set_shard); every iteration the partial product P = B(X)X (m*n_pad*d
 doubles) and the partial fidelity ride in one exchange buffer that must be
@@ -45,6 +49,26 @@ def attach_nccl(dev, d, group=None):
     dev.set_allreduce(hook)
     dev._xbuf = buf
     return buf
+
+
+def exchange_handles(handle, group=None):
+    """All-gather of one bytes object per rank (rank order)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, handle, group=group)
+    return out
+
+
+def attach_peers(dev, group=None):
+    """Peer-memory exchange instead of NCCL (jofc_peer_*): every rank exports
+    its slab as a CUDA IPC handle, the handles are all-gathered, every rank
+    maps the others' slabs.  The Guttman loop then exchanges products and
+    configuration rows through NVLink loads/stores inside its own kernels."""
+    import torch.distributed as dist
+    handle, _ = dev.peer_export()
+    handles = exchange_handles(handle, group)
+    dev.peer_attach(dist.get_rank(group), len(handles), handles)
+    return handles
 
 
 class ThreadGroup:

@@ -115,3 +115,69 @@ def test_sharded_step_gloo_matches_oracle(world):
         assert abs(sigma - ref_stress) / ref_stress < 1e-12
     # both ranks hold identical results (the all-reduce is the only exchange)
     assert np.array_equal(out[0][0], out[1][0])
+
+
+def _peer_worker(rank, world, port, payload, out):
+    # the peer exchange's decomposition (csrc/jofc_peer.cuh) restated over
+    # gloo: slab handles all-gathered; each rank sums ITS rows of every rank's
+    # partial products in rank order, mixes them and writes the rows to every
+    # rank; sigma = rank-order sum of the fidelity partials + rank-order sum of
+    # the per-rank commensurability
+    import torch
+    from paper_1502_03391_b200.dist import exchange_handles
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    handles = exchange_handles(bytes([rank + 1]) * 64)
+    assert handles == [bytes([q + 1]) * 64 for q in range(world)]
+    delta, x, within, coef, cross = payload
+    m, n, d = x.shape
+    P, fid = partial_products(delta, x, within, m, n, rank, world)
+    slabs = [torch.zeros(P.size + 1, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(slabs, torch.from_numpy(np.concatenate([P.ravel(), [fid]])))
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    S = np.zeros((m, hi - lo, d))
+    for q in range(world):
+        S += slabs[q].numpy()[:-1].reshape(m, n, d)[:, lo:hi]
+    rows = np.einsum("jl,lic->jic", coef, S)
+    com = sum(cross[a, b] * np.sum((x[a, lo:hi] - x[b, lo:hi]) ** 2)
+              for a in range(m) for b in range(a + 1, m))
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (lo, hi, rows, com))
+    xn = np.zeros_like(x)
+    for q_lo, q_hi, q_rows, _ in gathered:
+        xn[:, q_lo:q_hi] = q_rows
+    sigma = 0.0
+    for q in range(world):
+        sigma += float(slabs[q][-1])
+    comsum = 0.0
+    for *_, q_com in gathered:
+        comsum += q_com
+    out[rank] = (xn, sigma + comsum)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_peer_decomposition_gloo_matches_oracle(world):
+    from oracle.oracle import Port, Spec
+    P = Port()
+    rng = np.random.default_rng(6)
+    m, n, d = 3, 257, 2
+    delta = np.stack([P.distance_matrix(rng.normal(size=(n, 3))) for _ in range(m)])
+    x = rng.normal(size=(m, n, d))
+    spec = Spec.uniform(0.7)
+    within, cross = P.weights_expand(spec, m)
+    winv = P.script_w_inverse(spec, m, n)
+    coef = winv * within[None, :]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = 30500 + os.getpid() % 1000
+    mp.spawn(_peer_worker, args=(world, port, (delta, x, within, coef, cross), out),
+             nprocs=world, join=True)
+    ref_step = P.guttman_step_fast(delta, spec, x)
+    ref_stress = P.raw_stress(delta, spec, x)
+    for r in range(world):
+        xn, sigma = out[r]
+        assert np.linalg.norm(xn - ref_step) / np.linalg.norm(ref_step) < 1e-12
+        assert abs(sigma - ref_stress) / ref_stress < 1e-12
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
