@@ -353,16 +353,23 @@ def run_e2e(args, wl, dev, spec, world, rank, torch, dist, x_dev):
     its, conv = C.c_size_t(), C.c_int()
     steps = max(1, args.e2e_steps)
 
+    split = [0.0, 0.0]  # wall seconds in the upload / the solve call
+
     def one():
+        a = time.perf_counter()
         check(lib.jofc_set_problem(dev.h, wl.m, wl.n, ptrs, 0))
+        b = time.perf_counter()
         check(lib.jofc_fjofc_embed(dev.h, C.byref(spec.c()), wl.d, dptr(x0), 1e-300,
                                    wl.iterations, dptr(x_out), dptr(trace), C.byref(its),
                                    C.byref(conv), None))
+        split[0] += b - a
+        split[1] += time.perf_counter() - b
 
     one()  # warm-up
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    split[:] = [0.0, 0.0]
     t0 = time.perf_counter()
     for _ in range(steps):
         one()
@@ -382,6 +389,8 @@ def run_e2e(args, wl, dev, spec, world, rank, torch, dist, x_dev):
     return {"value": round(its.value * steps / sec, 3), "unit": "it/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
             "ms_per_step": round(sec / steps * 1e3, 2),
+            "upload_ms_per_step": round(split[0] / steps * 1e3, 2),
+            "solve_ms_per_step": round(split[1] / steps * 1e3, 2),
             "path": "jofc_set_problem(pinned dense host Delta) + jofc_fjofc_embed(host X0 -> "
                     "host X, trace); wall clock, synchronous C-ABI calls",
             "x_final_rel_diff_vs_device_run": float(np.linalg.norm(x_out - x_dev)

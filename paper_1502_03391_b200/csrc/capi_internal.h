@@ -201,6 +201,7 @@ struct jofc_ctx {
   // host -> device upload: copies on their own stream, overlapped with packing
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t up_copied[2] = {nullptr, nullptr}, up_packed[2] = {nullptr, nullptr};
+  DevBuf<int> up_bad;  // set by the pack kernel on a non-finite / negative entry
   // early stop of synchronous solves: the done flag every kStopChunk
   // iterations (pinned) and the events that say it has landed
   int* stop_flag = nullptr;

@@ -607,6 +607,7 @@ int jofc_ctx_destroy(jofc_ctx* c) {
                             &c->oos_y1, &c->oos_part, &c->oos_trace})
     b->release();
   c->ctrl.release();
+  c->up_bad.release();
   c->oos_st.release();
   for (auto& e : c->prof_events) {
     cudaEventDestroy(e.first);
@@ -728,8 +729,10 @@ int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta
       JOFC_CUDA(cudaEventCreateWithFlags(&c->up_packed[k], cudaEventDisableTiming));
     }
   }
-  DevBuf<double> stage[2];
-  DevBuf<int> bad;
+  // (device staging shared with file ingest, kept across uploads: no
+  // cudaMalloc / synchronising cudaFree per call)
+  DevBuf<double>* stage = c->ingest.stage;
+  DevBuf<int>& bad = c->up_bad;
   for (int k = 0; k < 2; ++k) JOFC_CUDA(stage[k].ensure(static_cast<size_t>(kChunk) * kRows * L.n_pad));
   JOFC_CUDA(bad.ensure(1));
   JOFC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
