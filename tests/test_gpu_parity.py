@@ -297,3 +297,44 @@ def test_oos_batch_config5(dev, P):
     for q in range(200):
         assert rel_fro(y[q], yr[q]) < X_TOL
         assert np.max(np.abs(tr[q] - trr[q]) / np.abs(trr[q])) < S_TOL
+
+
+def test_maximum_size_realizable_fixed_point(dev):
+    # n = 100000 (n^2 > 2^32, 40 GB of packed Delta built on the device from the
+    # features): for realizable data the configuration that generated Delta
+    # has zero fidelity and is a fixed point of the transform
+    # (B(X*) X* = n X* for centred X*; proj/tests/test_embed_core.cpp:277-292
+    # at maximum size)
+    rng = np.random.default_rng(77)
+    n, d = 100_000, 3
+    xs = rng.normal(size=(n, d)) * 10.0
+    xs -= xs.mean(axis=0)
+    prob = dev.upload_features(xs[None])
+    assert dev.problem_pairs() == n * (n - 1) / 2
+    u = jg.WeightSpec.uniform(1.0)
+    x = xs[None].copy()
+    scale = float(np.sum(xs * xs)) * n  # ~ sum of delta^2 over the pairs
+    assert jg.raw_stress(x, prob, u, device=dev) < 1e-24 * scale
+    step = jg.guttman_step_fast(x, prob, u, device=dev)
+    assert rel_fro(step, x) < 1e-13
+
+
+def test_maximum_size_oos_fixed_points(dev):
+    # out of sample at n = 200000 in-sample objects, m = 3, a batch of 64
+    # points: a point whose dissimilarities are its true distances to every
+    # modality's configuration (the same location in each) is a fixed point of
+    # the update (r_k = 1: psi = n, xi = 0) with zero stress
+    rng = np.random.default_rng(78)
+    m, n, d, k = 3, 200_000, 2, 64
+    x = rng.normal(size=(m, n, d)) * 5.0
+    ys = rng.normal(size=(k, d)) * 5.0
+    deltas = np.sqrt(((x[None, :, :, :] - ys[:, None, None, :]) ** 2).sum(-1))  # k x m x n
+    y0 = np.repeat(ys[:, None, :], m, axis=1)
+    y, traces, its = jg.oos_embed_batch(x, deltas, 0.5, y0, jg.OosOptions(eps=1e-300,
+                                                                          max_iterations=3),
+                                        fixed_iterations=True, device=dev)
+    assert np.all(its == 3)
+    assert np.max(np.abs(y - y0)) < 1e-12 * np.max(np.abs(y0))
+    assert np.all(traces[:, :4] < 1e-20 * n * 25.0)
+    assert jg.oos_stress(y0[0], x, deltas[0], 0.5, device=dev) < 1e-20 * n * 25.0
+    assert np.max(np.abs(jg.oos_step_fast(y0[5], x, deltas[5], 0.5, device=dev) - y0[5])) < 1e-12 * 5
