@@ -671,6 +671,9 @@ int jofc_set_shard(jofc_ctx* c, int rank, int world) {
   if (!c) return set_error(JOFC_EINVAL, "null context");
   if (world < 1 || rank < 0 || rank >= world)
     return set_error(JOFC_EINVAL, "shard %d of %d invalid", rank, world);
+  JOFC_CUDA(cudaSetDevice(c->device));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  peer_release(c);  // a new shard needs a new problem and a new peer group
   c->rank = rank;
   c->world = world;
   c->has_problem = false;
