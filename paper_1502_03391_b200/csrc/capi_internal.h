@@ -26,6 +26,9 @@ constexpr long long kFuseEpilogueMaxN = 1024;
 // Synchronous solves stop enqueuing iterations once the device says done,
 // checked every kStopChunk iterations (at most ~2 chunks of no-op launches).
 constexpr size_t kStopChunk = 32;
+// Largest packed block stream (all modalities) solved by the single-launch
+// persistent kernel on one GPU.
+constexpr long long kPersistentMaxBlocks = 4096;
 
 inline thread_local std::string g_error;
 

@@ -220,6 +220,37 @@ int jofc_gpu::capi::pass_for_d(jofc_ctx* c, const PassParams& pp) {
 
 namespace {
 
+// The whole solve as one cooperative launch (jofc_solve_persistent_kernel).
+template <int D>
+int launch_persistent(jofc_ctx* c, const PassParams& pp) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    JOFC_CUDA(cudaFuncSetAttribute(jofc_solve_persistent_kernel<D>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sizeof(PassSmem<D>))));
+    attr_done = true;
+  }
+  PassParams arg = pp;
+  void* args[] = {&arg};
+  JOFC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(jofc_solve_persistent_kernel<D>),
+                                        dim3(c->pass_grid), dim3(kPassThreads), args,
+                                        sizeof(PassSmem<D>), c->stream));
+  return JOFC_OK;
+}
+
+int persistent_for_d(jofc_ctx* c, const PassParams& pp) {
+  JOFC_DISPATCH_D(c->d, launch_persistent, c, pp);
+}
+
+// Single-launch solves for problems whose pass is short (JOFC_PERSISTENT=0/1
+// forces it off / on for experiments).
+bool use_persistent(const jofc_ctx* c) {
+  static const char* env = std::getenv("JOFC_PERSISTENT");
+  if (env && env[0] == '0') return false;
+  if (env && env[0] == '1') return true;
+  return c->lay.local() <= kPersistentMaxBlocks;
+}
+
 int setup_for_d(jofc_ctx* c) { JOFC_DISPATCH_D(c->d, setup_for, c); }
 int epi_for_d(jofc_ctx* c, const EpiParams& ep) { JOFC_DISPATCH_D(c->d, launch_epi, c, ep); }
 
@@ -282,9 +313,10 @@ int alloc_solve_state(jofc_ctx* c, size_t d, size_t max_it) {
   }
   c->pass_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(c->num_sms, L.local())));
   c->epi_grid = static_cast<int>((L.n + 255) / 256);
-  JOFC_CUDA(c->fid_part.ensure(c->pass_grid));
+  JOFC_CUDA(c->fid_part.ensure(2 * static_cast<size_t>(c->pass_grid)));
   JOFC_TRY(pass_bounds(c));
-  JOFC_CUDA(c->com_part.ensure(c->epi_grid));
+  // (the persistent kernel keeps one commensurability partial per pass CTA)
+  JOFC_CUDA(c->com_part.ensure(std::max(c->epi_grid, c->pass_grid)));
   JOFC_CUDA(c->trace.ensure(max_it + 1));
   JOFC_CUDA(c->ctrl.ensure(1));
   JOFC_CUDA(c->consts.ensure(3 * static_cast<size_t>(L.m) * L.m + L.m));
@@ -444,6 +476,12 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
     }
     return JOFC_OK;
   };
+  if (graphable && use_persistent(c)) {
+    JOFC_TRY(persistent_for_d(c, pp));
+    ++c->launches;
+    c->max_it_enqueued = max_it;
+    return JOFC_OK;
+  }
   if (graphable) {
     // one graph of the whole sequence, or (early stop) of one chunk replayed
     // until the device says done: later iterations are no-ops on the device
