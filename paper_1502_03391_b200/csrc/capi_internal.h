@@ -10,6 +10,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <map>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -57,6 +59,21 @@ inline int set_error(int code, const char* fmt, ...) {
   } while (0)
 
 constexpr int kMaxD = 10;
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: set it
+// once per (kernel, device) of the process.
+template <class K>
+cudaError_t ensure_smem_attr(K kernel, int bytes, int device) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), device);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             bytes);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
+}
 
 // FN<D>(args) for the runtime dimension d (1..kMaxD)
 #define JOFC_DISPATCH_D(d, FN, ...)         \

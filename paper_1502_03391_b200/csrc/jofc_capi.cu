@@ -178,19 +178,14 @@ namespace {
 size_t fid_slot(const jofc_ctx* c) { return static_cast<size_t>(c->lay.m) * c->lay.n_pad * c->d; }
 
 template <int D>
-int setup_pass() {
-  static bool attr_done = false;
-  if (!attr_done) {
-    JOFC_CUDA(cudaFuncSetAttribute(jofc_pass_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(sizeof(PassSmem<D>))));
-    attr_done = true;
-  }
+int setup_pass(int device) {
+  JOFC_CUDA(ensure_smem_attr(jofc_pass_kernel<D>, static_cast<int>(sizeof(PassSmem<D>)), device));
   return JOFC_OK;
 }
 
 template <int D>
 int launch_pass(jofc_ctx* c, const PassParams& pp) {
-  int rc = setup_pass<D>();
+  int rc = setup_pass<D>(c->device);
   if (rc) return rc;
   jofc_pass_kernel<D><<<c->pass_grid, kPassThreads, sizeof(PassSmem<D>), c->stream>>>(pp);
   JOFC_CUDA(cudaGetLastError());
@@ -198,8 +193,8 @@ int launch_pass(jofc_ctx* c, const PassParams& pp) {
 }
 
 template <int D>
-int setup_for(jofc_ctx*) {
-  return setup_pass<D>();
+int setup_for(jofc_ctx* c) {
+  return setup_pass<D>(c->device);
 }
 
 template <int D>
@@ -223,13 +218,8 @@ namespace {
 // The whole solve as one cooperative launch (jofc_solve_persistent_kernel).
 template <int D>
 int launch_persistent(jofc_ctx* c, const PassParams& pp) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    JOFC_CUDA(cudaFuncSetAttribute(jofc_solve_persistent_kernel<D>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(sizeof(PassSmem<D>))));
-    attr_done = true;
-  }
+  JOFC_CUDA(ensure_smem_attr(jofc_solve_persistent_kernel<D>,
+                             static_cast<int>(sizeof(PassSmem<D>)), c->device));
   PassParams arg = pp;
   void* args[] = {&arg};
   JOFC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(jofc_solve_persistent_kernel<D>),
