@@ -467,10 +467,14 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
     return JOFC_OK;
   };
   if (graphable && use_persistent(c)) {
-    JOFC_TRY(persistent_for_d(c, pp));
-    ++c->launches;
-    c->max_it_enqueued = max_it;
-    return JOFC_OK;
+    // (a cooperative launch is refused when the SMs are shared, e.g. under
+    // MPS: the per-iteration launches below then run the solve)
+    if (persistent_for_d(c, pp) == JOFC_OK) {
+      ++c->launches;
+      c->max_it_enqueued = max_it;
+      return JOFC_OK;
+    }
+    cudaGetLastError();
   }
   if (graphable) {
     // one graph of the whole sequence, or (early stop) of one chunk replayed
