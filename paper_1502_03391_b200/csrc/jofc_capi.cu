@@ -272,6 +272,14 @@ int pass_bounds(jofc_ctx* c) {
   for (double v : cost) total += v;
   std::vector<long long> b(NG + 1, L.end);
   b[0] = L.begin;
+  if (L.local() <= NG) {  // one block per CTA (cost cuts would pair some up)
+    for (int i = 0; i <= NG; ++i) b[i] = std::min(L.end, L.begin + i);
+    JOFC_CUDA(c->bounds.ensure(NG + 1));
+    JOFC_TRY(copy_sync(c, c->bounds.p, b.data(), (NG + 1) * sizeof(long long),
+                       cudaMemcpyHostToDevice));
+    c->bounds_key = key;
+    return JOFC_OK;
+  }
   double acc = 0.0;
   int cut = 1;
   for (size_t i = 0; i < cost.size() && cut < NG; ++i) {
@@ -865,6 +873,7 @@ int jofc_fetch_result(jofc_ctx* c, double* x_out, double* trace_out, size_t* ite
                       int* converged) {
   int rc = require_problem(c);
   if (rc) return rc;
+  if (!c->ctrl.p) return set_error(JOFC_EINVAL, "fetch: no solve was enqueued");
   Control h;
   rc = finish_solve(c, &h);
   if (rc) return rc;
