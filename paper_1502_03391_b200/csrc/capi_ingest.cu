@@ -3,6 +3,7 @@
 #include <omp.h>
 #include <unistd.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -36,8 +37,16 @@ struct InputCheck {
   std::vector<std::pair<long long, double>> diag;  // nonzero diagonal entries
 };
 
+// True if some entry of v[0, cols) is negative, NaN or infinite: one
+// branch-free (vectorisable) pass; the exact position is searched only then.
+bool row_has_bad(const double* v, long long cols) {
+  int bad = 0;
+  for (long long j = 0; j < cols; ++j) bad |= !(v[j] >= 0.0 && v[j] <= 1.7976931348623157e308);
+  return bad != 0;
+}
+
 void check_row(InputCheck& ck, long long r, const double* v, long long cols) {
-  if (!ck.bad)
+  if (!ck.bad && row_has_bad(v, cols))
     for (long long j = 0; j < cols; ++j) {
       const double x = v[j];
       if (!std::isfinite(x) || x < 0.0) {
@@ -54,6 +63,8 @@ void check_row(InputCheck& ck, long long r, const double* v, long long cols) {
 
 int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize) {
   using namespace ingest;
+  using clk = std::chrono::steady_clock;
+  const auto t_call = clk::now();
   if (paths.empty()) return set_error(JOFC_EINVAL, "load_dissimilarities: no input files");
   const std::string& p0 = paths.front();
   const bool binary = paths.size() == 1 && p0.size() >= 5 && p0.compare(p0.size() - 5, 5, ".jofc") == 0;
@@ -90,7 +101,7 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
   // panels of whole row blocks, ~64 MB each
   const long long panel_rows =
       std::max<long long>(1, (64LL << 20) / (8LL * std::max<long long>(n, 1)) / kRows) * kRows;
-  DevBuf<unsigned long long> keys;
+  DevBuf<unsigned long long>& keys = c->ingest_keys;  // first asymmetric pair per modality
   IngestPanels& pin = c->ingest;
   if (device) {
     make_layout(c, static_cast<size_t>(m), static_cast<size_t>(n));
@@ -145,8 +156,18 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
     }
     return JOFC_OK;
   };
+  // JOFC_INGEST_TRACE=1: seconds spent reading + checking, waiting for a free
+  // panel, enqueuing copies/kernels, and in the final synchronisation (stderr)
+  static const bool trace = std::getenv("JOFC_INGEST_TRACE") != nullptr;
+  double t_read = 0.0, t_wait = 0.0, t_flush = 0.0;
+  const auto t_begin = clk::now();
+  auto since = [](clk::time_point a) {
+    return std::chrono::duration<double>(clk::now() - a).count();
+  };
   auto acquire = [&](int k) -> int {  // host panel k free again (its last copy landed)
+    const auto a = clk::now();
     if (panels >= 2) JOFC_CUDA(cudaEventSynchronize(pin.copied[k]));
+    t_wait += since(a);
     return JOFC_OK;
   };
 
@@ -170,6 +191,7 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
         }
         // parallel positioned reads + entry checks, one slab of rows per thread
         const int nt = std::max(1, std::min(16, omp_get_max_threads()));
+        const auto t_r0 = clk::now();
         std::vector<InputCheck> part(nt);
         int io_err = 0;
 #pragma omp parallel num_threads(nt)
@@ -192,6 +214,7 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
           if (done == bytes)
             for (long long i = a; i < b; ++i) check_row(part[t], r0 + i, dst + i * n, n);
         }
+        t_read += since(t_r0);
         if (io_err) return set_error(JOFC_EINVAL, "'%s': truncated payload", p0.c_str());
         for (const InputCheck& pc : part) {  // merge in row order
           if (pc.bad && !ck.bad) {
@@ -204,8 +227,10 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
           ck.diag.insert(ck.diag.end(), pc.diag.begin(), pc.diag.end());
         }
         if (device && !ck.bad) {
+          const auto t_f0 = clk::now();
           rc = flush(k, static_cast<int>(l), r0, rows);
           if (rc) return rc;
+          t_flush += since(t_f0);
           ++panels;
         }
       }
@@ -302,7 +327,13 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
       c->launches += 2;
     }
   }
+  const auto t_s0 = clk::now();
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  if (trace)
+    std::fprintf(stderr, "ingest: %lld panels, read+check %.2f ms, wait %.2f ms, enqueue %.2f ms, "
+                 "final sync %.2f ms, pipeline %.2f ms, call %.2f ms\n", panels, t_read * 1e3,
+                 t_wait * 1e3, t_flush * 1e3, since(t_s0) * 1e3, since(t_begin) * 1e3,
+                 since(t_call) * 1e3);
   c->has_problem = true;
   return JOFC_OK;
 }

@@ -218,6 +218,7 @@ struct jofc_ctx {
   DevBuf<unsigned> oos_done;
   // streaming ingest staging
   IngestPanels ingest;
+  DevBuf<unsigned long long> ingest_keys;
   // host -> device upload: copies on their own stream, overlapped with packing
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t up_copied[2] = {nullptr, nullptr}, up_packed[2] = {nullptr, nullptr};

@@ -648,6 +648,7 @@ int jofc_ctx_destroy(jofc_ctx* c) {
     b->release();
   c->ctrl.release();
   c->up_bad.release();
+  c->ingest_keys.release();
   c->oos_st.release();
   for (auto& e : c->prof_events) {
     cudaEventDestroy(e.first);
