@@ -19,7 +19,11 @@
 namespace jofc_gpu {
 namespace ingest {
 
-// Line-oriented CSV row reader.
+// CSV row reader.  Text is read in large batches of whole lines, split at
+// line boundaries over the host threads and parsed in parallel; rows are
+// then handed out one by one in file order, and a parse error surfaces at
+// its place in that order (after every row before it), exactly as a
+// line-by-line reader would report it.
 class CsvRows {
  public:
   ~CsvRows();
@@ -31,14 +35,29 @@ class CsvRows {
   size_t line() const { return lineno_; }  // number of the last line read
 
  private:
+  // One thread's share of a batch: its parsed rows, and where it stopped.
+  struct Part {
+    std::vector<double> vals;
+    std::vector<size_t> off;    // row r = vals[off[r], off[r + 1])
+    std::vector<size_t> line;   // line number of row r within the batch part
+    size_t lines = 0;           // lines scanned (up to and including an error line)
+    bool failed = false;
+    std::string bad_field;      // the field that failed to parse
+  };
   bool fill();
+  bool parse_batch();  // next batch of whole lines -> parts_; false at end of file
   std::FILE* f_ = nullptr;
   std::string path_;
   std::vector<char> buf_;
   size_t pos_ = 0, len_ = 0;
+  size_t file_off_ = 0;    // bytes of the file read so far
   bool eof_ = false;
-  size_t lineno_ = 0;
-  std::string line_;
+  size_t lineno_ = 0;      // line of the last row handed out
+  size_t batch_base_ = 0;  // lines before the current batch
+  std::vector<Part> parts_;
+  std::vector<size_t> part_base_;  // lines before each part (within the batch)
+  size_t cur_part_ = 0, cur_row_ = 0;
+  bool have_batch_ = false;
 };
 
 struct JofcHeader {

@@ -253,3 +253,26 @@ def test_sharded_load_matches_single(tmp_path, world):
     assert not errors, errors
     for r in range(world):
         np.testing.assert_allclose(out[r], ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+
+
+def test_errors_deep_in_large_csv_match_reference(R, dev, tmp_path):
+    # 2000 x 2000 CSVs (~80 MB: several 32 MB text batches, each split over the
+    # host threads) with blank lines: the first bad line must be reported with
+    # the reference's line number, after every row before it
+    a = deltas(2000, m=1, seed=9)[0]
+    rows = [",".join("%.17g" % v for v in r) for r in a]
+    for name, mutate in (("parse", lambda r: r.replace(",", ",1.2.3,", 1)),
+                         ("ragged", lambda r: r.rsplit(",", 1)[0])):
+        for at in (1, 777, 1999):
+            lines = []
+            for i, r in enumerate(rows):
+                if i % 7 == 3:
+                    lines.append("   ")
+                lines.append(mutate(r) if i == at else r)
+            p = tmp_path / f"{name}_{at}.csv"
+            p.write_text("\n".join(lines) + "\n")
+            with pytest.raises(ValueError) as ref_e:
+                R.load_dissimilarities([str(p)])
+            with pytest.raises(jg.InvalidArgument) as our_e:
+                jg.load_dissimilarities([str(p)], device=dev)
+            assert str(our_e.value) == ref_e.value.args[-1], (name, at)
