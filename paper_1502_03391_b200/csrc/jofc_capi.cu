@@ -600,6 +600,11 @@ int jofc_gpu::capi::finish_solve(jofc_ctx* c, Control* out) {
     c->peer.phase = (c->peer.phase + last + 1) & 1;
     c->peer.pending = false;
   }
+  if (out->status == 3) {
+    peer_release(c);  // the group's exchange state is unknown: attach again
+    return set_error(JOFC_ECOMM, "peer exchange: a rank did not arrive within 20 s (iteration %d)",
+                     out->err_iter);
+  }
   if (out->status == 2) {
     if (out->err_iter == 0)
       return set_error(JOFC_ENUMERIC, "embed: non-finite stress at the initial configuration");

@@ -60,8 +60,31 @@ struct PeerParams {
   long long fid_slot;
 };
 
-__device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long target) {
-  while (ld_acquire_sys(f) < target) __nanosleep(32);
+// A rank that never arrives fails the solve instead of hanging it: after
+// kPeerTimeoutNs of polling the waiting kernel marks the control block
+// (status 3, done) and returns; finish_solve reports JOFC_ECOMM.
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+
+__device__ __forceinline__ bool wait_flag(const unsigned long long* f, unsigned long long target) {
+  if (ld_acquire_sys(f) >= target) return true;
+  const unsigned long long t0 = global_ns();
+  while (ld_acquire_sys(f) < target) {
+    __nanosleep(32);
+    if (global_ns() - t0 > kPeerTimeoutNs) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void peer_timeout(Control* ctrl, int t) {
+  ctrl->status = 3;
+  ctrl->err_iter = t;
+  ctrl->done = 1;
 }
 
 template <int D>
@@ -71,13 +94,21 @@ __global__ void __launch_bounds__(256) jofc_peer_mix_kernel(const PeerParams p) 
   extern __shared__ double s_sum[];  // [m][rows_cta * D]: the world's P for this CTA's objects
   __shared__ double red[8];
   __shared__ bool last;
+  __shared__ int timed_out;
   const int t = ctrl->t;
   const unsigned long long target = flag_value(ctrl->epoch, t);
   double* own = p.slabs[p.rank];
-  if (threadIdx.x < p.world)
-    wait_flag(reinterpret_cast<const unsigned long long*>(own + p.flag1_off) + threadIdx.x,
-              target);
+  if (threadIdx.x == 0) timed_out = 0;
   __syncthreads();
+  if (threadIdx.x < p.world &&
+      !wait_flag(reinterpret_cast<const unsigned long long*>(own + p.flag1_off) + threadIdx.x,
+                 target))
+    timed_out = 1;
+  __syncthreads();
+  if (timed_out) {
+    if (threadIdx.x == 0) peer_timeout(ctrl, t);
+    return;
+  }
 
   const long long i0 = p.row_lo + static_cast<long long>(blockIdx.x) * p.rows_cta;
   const int rows = static_cast<int>(
@@ -162,10 +193,15 @@ static __global__ void __launch_bounds__(32) jofc_peer_decide_kernel(const PeerP
   const double* own = p.slabs[p.rank];
   double f = 0.0, c = 0.0;
   const int q = threadIdx.x;
+  bool ok = true;
   if (q < p.world) {
-    wait_flag(reinterpret_cast<const unsigned long long*>(own + p.flag2_off) + q, target);
+    ok = wait_flag(reinterpret_cast<const unsigned long long*>(own + p.flag2_off) + q, target);
     f = ld_relaxed_sys(p.slabs[q] + p.p_read + p.fid_slot);
     c = ld_relaxed_sys(p.slabs[q] + p.com_off);
+  }
+  if (!__all_sync(0xffffffffu, ok)) {
+    if (threadIdx.x == 0) peer_timeout(ctrl, t);
+    return;
   }
   double fid = 0.0, com = 0.0;
   for (int r = 0; r < p.world; ++r) {

@@ -117,3 +117,16 @@ def test_peer_export_and_attach_checks():
                           init_config=wl.x0())
     with pytest.raises(jg.CommError):
         jg.fjofc_embed(prob, wl.spec, opt, device=dv)
+
+
+def test_peer_missing_rank_fails_loudly():
+    # rank 1 never runs: rank 0's exchange kernel gives up after its 20 s
+    # timeout and the solve raises instead of hanging (no kernel waits on a
+    # running kernel: the other rank is simply absent)
+    wl = workloads.make(1, n=200)
+    prob = jg.OmnibusProblem(list(wl.dense_delta()), validate=False)
+    devs = group(prob, 2)
+    opt = jg.SolveOptions(dim=wl.d, eps=1e-300, max_iterations=2, init=jg.InitKind.provided,
+                          init_config=wl.x0())
+    with pytest.raises(jg.CommError, match="did not arrive"):
+        jg.fjofc_embed(prob, wl.spec, opt, device=devs[0])
