@@ -496,7 +496,9 @@ def run_reference(args):
 # ------------------------------------------------------------ out-of-sample
 def run_oos(args):
     """C5 out-of-sample: k = 1000 new objects embedded against the frozen
-    in-sample configuration, batched, 100 fixed Guttman updates per step."""
+    in-sample configuration, batched, 100 fixed Guttman updates per step.
+    Under torchrun the points are split over the ranks (independent units,
+    SURVEY.md 8e: no collective in the loop); time = max over ranks."""
     import ctypes as C
 
     import torch
@@ -505,10 +507,26 @@ def run_oos(args):
     from paper_1502_03391_b200 import workloads
     from paper_1502_03391_b200._capi import check, dptr
 
+    import torch.distributed as dist
+
     rank, world, local = env_rank()
-    if rank != 0:
-        return
+    local = rank_device(local, torch)
     torch.cuda.set_device(local)
+    if world > 1:
+        init_dist(local, torch, dist)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
     wl = workloads.make(5)
     dev = jg.Device(local)
     lib = dev.lib
@@ -521,9 +539,11 @@ def run_oos(args):
     its = C.c_size_t()
     conv = C.c_int()
     check(lib.jofc_fetch_result(dev.h, dptr(xin), None, C.byref(its), C.byref(conv)))
-    k, m, n, d, T = wl.oos_points, wl.m, wl.n, wl.d, 100
-    od = wl.oos_deltas()
-    y0 = np.stack([jg.oos_start(xin, workloads.OOS_SEED + q) for q in range(k)])
+    k_all, m, n, d, T = wl.oos_points, wl.m, wl.n, wl.d, 100
+    q_lo, q_hi = k_all * rank // world, k_all * (rank + 1) // world  # this rank's points
+    k = q_hi - q_lo
+    od = np.ascontiguousarray(wl.oos_deltas()[q_lo:q_hi])
+    y0 = np.stack([jg.oos_start(xin, workloads.OOS_SEED + q) for q in range(q_lo, q_hi)])
     xs = torch.from_numpy(xin).cuda()
     ods = torch.from_numpy(od).cuda()
     y0s = torch.from_numpy(y0).cuda()
@@ -539,15 +559,19 @@ def run_oos(args):
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
+    barrier()
     launches0 = dev.launches()
     clocks = ClockSampler(local)
     clocks.start()
-    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.ExternalStream(dev.stream)
+    e0.record(stream)
     for _ in range(args.steps):
         step()
-    torch.cuda.synchronize()
-    sec = time.perf_counter() - t0
+    e1.record(stream)
+    e1.synchronize()
+    sec = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+    barrier()
     clk = clocks.stop()
     launches = dev.launches() - launches0
     value = T * args.steps / sec
@@ -560,18 +584,22 @@ def run_oos(args):
               if int(cudart.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)) == 0]
     check(lib.jofc_oos_batch(dev.h, k, m, n, d, dptr(xin), dptr(od), wl.w, dptr(y0), 1e-300,
                              T, 1, dptr(yh), None, None))  # warm-up
+    barrier()
     t0 = time.perf_counter()
     e2e_steps = max(1, args.e2e_steps)
     for _ in range(e2e_steps):
         check(lib.jofc_oos_batch(dev.h, k, m, n, d, dptr(xin), dptr(od), wl.w, dptr(y0), 1e-300,
                                  T, 1, dptr(yh), None, None))
-    e2e = T * e2e_steps / (time.perf_counter() - t0)
+    e2e = T * e2e_steps / max_over_ranks(time.perf_counter() - t0)
     for arr in pinned:
         cudart.cudaHostUnregister(arr.ctypes.data)
     hbm_peak, hbm_src = measured_peaks()
     bytes_per_it = od.nbytes
+    if rank != 0:
+        dev.close()
+        return
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         from oracle.oracle import Port, Reference
         try:
             R, kind = Reference(), "reference"
@@ -581,24 +609,27 @@ def run_oos(args):
         t0 = time.perf_counter()
         R.oos_batch(xin, od[:sample], wl.w, y0[:sample], 1e-300, T, fixed=True)
         csec = time.perf_counter() - t0
-        cpu = {"value": round(T * sample / k / csec, 4), "unit": "batch-it/s", "kind": kind,
+        cpu = {"value": round(T * sample / k_all / csec, 4), "unit": "batch-it/s", "kind": kind,
                "cores": R.max_threads() if kind == "reference" else os.cpu_count(),
                "sample": f"{sample} of {k} points x {T} oos_step_fast+oos_stress "
                          f"(reference functions, OpenMP over points), scaled to the batch",
                "seconds": round(csec, 3)}
     line = {
-        "metric": f"OOS Guttman iterations/s of a {k}-point batch (fJOFC C5: m={m} n={n} d={d})",
-        "value": round(value, 2), "unit": "batch-it/s", "n_gpus": 1, "steps": args.steps,
+        "metric": f"OOS Guttman iterations/s of a {k_all}-point batch (fJOFC C5: m={m} n={n} d={d})",
+        "value": round(value, 2), "unit": "batch-it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(sec / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md)",
-        "config": {"workload": f"C5-OOS k={k} new objects, {T} fixed updates/step, "
+        "config": {"workload": f"C5-OOS k={k_all} new objects, {T} fixed updates/step, "
                                f"X from a 100-iteration GPU in-sample solve",
+                   "parallelism": (f"points split over {world} ranks, no collective in the "
+                                   f"loop" if world > 1 else "single"),
                    "l2": "delta rows 80 MB fit in the 126 MB L2 (re-read every update)"},
-        "point_iterations_per_s": round(value * k, 1),
+        "point_iterations_per_s": round(value * k_all, 1),
         "roofline": {"bound": "hbm", "achieved": round(bytes_per_it * value / 1e9, 1),
                      "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(bytes_per_it * value / 1e9 / hbm_peak, 4), "traffic": None,
+                     "per": "rank 0's GPU (its share of the delta rows)",
                      "peak_source": hbm_src, "kernel": "jofc_oos_pass_kernel + update",
                      "note": "whole update (pass + update kernel) per 80 MB of delta rows; "
                              "L2-resident, so HBM is not the binding roof"},

@@ -41,3 +41,21 @@ def test_bench_torchrun_two_ranks_share_one_gpu():
     assert out["value"] > 0 and out["gpu_launches"] > 0
     # the sharded solve through the host-buffer path ends on the device-run iterate
     assert out["e2e"]["x_final_rel_diff_vs_device_run"] < 1e-12
+
+
+def test_bench_oos_points_split_over_two_ranks():
+    # the out-of-sample leg under torchrun: each rank embeds its half of the
+    # 1000 points (independent units, no collective in the loop); rank 0 alone
+    # prints the whole-batch rate (time = max over ranks)
+    env = dict(os.environ, JOFC_DIST_BACKEND="gloo", JOFC_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--oos", "--steps", "2",
+           "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["value"] > 0
+    assert "2 ranks" in out["config"]["parallelism"]
