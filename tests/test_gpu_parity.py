@@ -338,3 +338,26 @@ def test_maximum_size_oos_fixed_points(dev):
     assert np.all(traces[:, :4] < 1e-20 * n * 25.0)
     assert jg.oos_stress(y0[0], x, deltas[0], 0.5, device=dev) < 1e-20 * n * 25.0
     assert np.max(np.abs(jg.oos_step_fast(y0[5], x, deltas[5], 0.5, device=dev) - y0[5])) < 1e-12 * 5
+
+
+def test_many_modalities(dev, P):
+    # m = 16 modalities (the epilogue's m x m mix and m(m-1)/2 commensurability
+    # pairs, product weights) against the port, steps and a short solve
+    rng = np.random.default_rng(66)
+    m, n, d = 16, 150, 3
+    z = rng.normal(size=(n, 3))
+    delta = np.stack([P.distance_matrix(z + 0.3 * rng.normal(size=(n, 3))) for _ in range(m)])
+    x = rng.normal(size=(m, n, d))
+    within = np.linspace(0.5, 2.0, m)
+    spec_o, spec = Spec.product(within, 0.8), jg.WeightSpec.product(within, 0.8)
+    prob = as_problem(delta)
+    assert rel(jg.raw_stress(x, prob, spec, device=dev), P.raw_stress(delta, spec_o, x)) < STEP_TOL
+    assert rel_fro(jg.guttman_step_fast(x, prob, spec, device=dev),
+                   P.guttman_step_fast(delta, spec_o, x)) < STEP_TOL
+    opt = jg.SolveOptions(dim=d, eps=1e-300, max_iterations=30, init=jg.InitKind.provided,
+                          init_config=x)
+    r = jg.fjofc_embed(prob, spec, opt, device=dev)
+    ref = P.fjofc_embed(delta, spec_o, x, 1e-300, 30)
+    assert r.iterations == ref.iterations
+    assert rel_fro(r.config, ref.x) < X_TOL
+    assert trace_close(r.stress_trace, ref.trace)
