@@ -698,15 +698,23 @@ def run_init(args):
     delta = wl.dense_delta() if not (args.no_e2e and args.no_cpu_baseline) else None
     if not args.no_e2e:
         mods = list(delta)
+        # the host Delta page-locked once outside the timed region, as the
+        # in-sample e2e does
+        cudart = torch.cuda.cudart()
+        pinned = int(cudart.cudaHostRegister(delta.ctypes.data, delta.nbytes, 0)) == 0
         e2e_steps = max(1, args.e2e_steps)
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             prob = jg.OmnibusProblem(mods, validate=False)
             jg.averaged_procrustes_init(prob, d, device=dev)
         e2e_sec = (time.perf_counter() - t0) / e2e_steps
+        if pinned:
+            cudart.cudaHostUnregister(delta.ctypes.data)
         e2e = {"value": round(1.0 / e2e_sec, 4), "unit": "inits/s",
-               "h2d_bytes_per_step": int(sum(x.nbytes for x in mods)),
-               "d2h_bytes_per_step": int(out.nbytes)}
+               "h2d_bytes_per_step": h2d_bytes_dense_upload(m, n, 1, 0),
+               "d2h_bytes_per_step": int(out.nbytes),
+               "path": "OmnibusProblem(host Delta) -> averaged_procrustes_init (upload of the "
+                       "upper part + the whole init + X back)"}
     cpu = None
     if not args.no_cpu_baseline:
         from oracle.oracle import Port, Reference
