@@ -130,6 +130,8 @@ int eigen_top_device(jofc_ctx* c, const double* S_dev, long long n, size_t k, do
     JOFC_CUDA(dw.ensure(n * p));
     JOFC_CUDA(dritz.ensure(n * k));
     JOFC_CUDA(dpart.ensure(grid * std::max(part1, part2)));
+    DevBuf<double> dsum;  // the per-CTA partials summed on the device (CTA order)
+    JOFC_CUDA(dsum.ensure(std::max(part1, part2)));
     // pinned staging for the per-CTA partials (two small D2H reads per sweep)
     struct Pinned {
       double* p = nullptr;
@@ -140,19 +142,23 @@ int eigen_top_device(jofc_ctx* c, const double* S_dev, long long n, size_t k, do
     JOFC_CUDA(cudaMallocHost(&hpart.p, grid * std::max(part1, part2) * sizeof(double)));
     JOFC_CUDA(cudaMemcpyAsync(dq.p, q.a.data(), q.a.size() * sizeof(double),
                               cudaMemcpyHostToDevice, c->stream));
+    // per-CTA partials -> one vector on the device (summed in CTA order, as the
+    // host did) -> the host: `per` doubles per fetch instead of blocks x per
     auto fetch = [&](int blocks, size_t per) -> int {
       JOFC_CUDA(cudaGetLastError());
+      init::sum_partials_kernel<<<static_cast<unsigned>((per + 255) / 256), 256, 0, c->stream>>>(
+          dpart.p, blocks, static_cast<int>(per), dsum.p);
+      JOFC_CUDA(cudaGetLastError());
+      ++c->launches;
       const auto t0 = clk::now();
-      JOFC_CUDA(cudaMemcpyAsync(hpart.p, dpart.p, blocks * per * sizeof(double),
-                                cudaMemcpyDeviceToHost, c->stream));
+      JOFC_CUDA(cudaMemcpyAsync(hpart.p, dsum.p, per * sizeof(double), cudaMemcpyDeviceToHost,
+                                c->stream));
       JOFC_CUDA(cudaStreamSynchronize(c->stream));
       t_sync += std::chrono::duration<double>(clk::now() - t0).count();
       return JOFC_OK;
     };
-    auto sum_part = [&](int blocks, size_t per, size_t off, size_t cnt, std::vector<double>& out) {
-      out.assign(cnt, 0.0);
-      for (int b = 0; b < blocks; ++b)
-        for (size_t e = 0; e < cnt; ++e) out[e] += hpart.p[b * per + off + e];
+    auto sum_part = [&](int, size_t, size_t off, size_t cnt, std::vector<double>& out) {
+      out.assign(hpart.p + off, hpart.p + off + cnt);
     };
     bool done = false;
     std::vector<double> acc;

@@ -150,6 +150,26 @@ static __global__ void __launch_bounds__(256) double_center_kernel(double* __res
   }
 }
 
+// out[e] = sum over b of part[b * per + e], b ascending (the order the host
+// summed the per-CTA partials in).
+static __global__ void __launch_bounds__(256) sum_partials_kernel(const double* __restrict__ part,
+                                                               int blocks, int per,
+                                                               double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= per) return;
+  double s = 0.0;
+  int b = 0;
+  for (; b + 16 <= blocks; b += 16) {  // 16 loads in flight, then the in-order adds
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldcg(part + static_cast<long long>(b + u) * per + e);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s += v[u];
+  }
+  for (; b < blocks; ++b) s += __ldcg(part + static_cast<long long>(b) * per + e);
+  out[e] = s;
+}
+
 // ------------------------------------------------- device subspace iteration
 // The n x p panels (Q, Z = S Q, W = Z + shift Q) stay in HBM; only p x p
 // Gram/Ritz matrices and per-CTA partial sums cross to the host each sweep.
