@@ -32,7 +32,7 @@ exp:
 	$(NVCC) $(NVFLAGS) $(EXP) -shared -o $(PKG)/libjofc_gpu_exp.so $(GPU_SRC) -lgomp
 
 $(PKG)/libjofc.so: $(DROPIN_SRC) $(DROPIN_HDR) $(PKG)/libjofc_gpu.so
-	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(DROPIN_SRC) \
+	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -I$(CSRC) -o $@ $(DROPIN_SRC) \
 	    -L$(PKG) -ljofc_gpu -Wl,-rpath,'$$ORIGIN'
 
 oracle:

@@ -5,12 +5,14 @@
 // bit-for-bit to the reference by tests/test_oracle.py.  Exit code = failures.
 #include <cmath>
 #include <cstdio>
+#include <fstream>
 #include <limits>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "jofc/init.hpp"
+#include "jofc/io.hpp"
 #include "jofc/linalg.hpp"
 #include "jofc/oos.hpp"
 #include "jofc/rng.hpp"
@@ -360,6 +362,66 @@ static void linear_algebra() {
   CHECK(max_abs_mat(orthogonal_procrustes(src, tgt), tgt) < 1e-12);
 }
 
+// load_dissimilarities over CSV (proj/src/io.cpp:127-215): values round-trip
+// exactly through %.17g text with blank lines, padding and CRLF; errors carry
+// the reference's wording and the line of the first bad row (the GPU ingest
+// suite, tests/test_gpu_ingest.py, compares the same strings with the reference).
+static std::string write_text(const std::string& name, const std::string& body) {
+  const std::string path = "/tmp/jofc_dropin_" + name;
+  std::ofstream(path, std::ios::binary) << body;
+  return path;
+}
+
+static std::string message_of(const std::vector<std::string>& paths) {
+  try {
+    load_dissimilarities(paths);
+  } catch (const std::invalid_argument& e) {
+    return e.what();
+  }
+  return "";
+}
+
+static void io_csv() {
+  Rng rng(91);
+  const std::size_t n = 700;  // ~13 MB of text per file: several parser threads
+  DenseMatrix z = random_matrix(rng, n, 3);
+  DenseMatrix d = edm(z);
+  std::string body;
+  char buf[64];
+  for (std::size_t i = 0; i < n; ++i) {
+    if (i % 97 == 5) body += "   \r\n";
+    for (std::size_t j = 0; j < n; ++j) {
+      std::snprintf(buf, sizeof buf, "%s %.17g", j ? "," : "", d(i, j));
+      body += buf;
+    }
+    body += (i % 2) ? "\r\n" : "\n";
+  }
+  const std::string a = write_text("a.csv", body), b = write_text("b.csv", body);
+  OmnibusProblem p = load_dissimilarities({a, b});
+  CHECK(p.modality_count() == 2 && p.object_count() == n);
+  bool same = true;
+  for (std::size_t l = 0; l < 2; ++l)
+    for (std::size_t i = 0; i < n * n; ++i) same &= p.modality(l).data()[i] == d.data()[i];
+  CHECK(same);
+  // the first bad line wins, in file order
+  std::string bad_body = body;
+  const std::size_t at = bad_body.find('\n', bad_body.size() / 2) + 1;  // a line start
+  bad_body.insert(at, "0,x");  // a bad number joined to the next row
+  const std::string bp = write_text("bad.csv", bad_body);
+  const std::string msg = message_of({bp});
+  CHECK(msg.find("'" + bp + "' line ") == 0);
+  CHECK(msg.find(": cannot parse number '") != std::string::npos);
+  std::size_t line = 1;
+  for (std::size_t i = 0; i < at; ++i) line += bad_body[i] == '\n';
+  CHECK(msg.find(" line " + std::to_string(line) + ":") != std::string::npos);
+  const std::string rg = write_text("ragged.csv", "0,1,2\n1,0\n2,1,0\n");
+  CHECK(message_of({rg}) == "'" + rg + "' line 2: ragged row");
+  const std::string em = write_text("empty.csv", "\n  \n");
+  CHECK(message_of({em}) == "'" + em + "': empty matrix");
+  CHECK(message_of({"/tmp/jofc_dropin_missing.csv"}) ==
+        "cannot open '/tmp/jofc_dropin_missing.csv'");
+}
+
 int main() {
   fast_step_grid();
   solve_trajectory();
@@ -368,6 +430,7 @@ int main() {
   errors();
   out_of_sample();
   linear_algebra();
+  io_csv();
   std::printf("dropin_parity: %d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
