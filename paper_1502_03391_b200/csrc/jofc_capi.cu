@@ -5,6 +5,8 @@
 // control block, and the launch sequence
 //
 //     for t = 0 .. max_it:   pass(t) -> [all-reduce hook] -> epilogue(t)
+//     (peer exchange:        pass(t) -> peer mix(t) -> peer decide(t), capi_peer.cu)
+//     (small, one GPU:       one jofc_solve_persistent_kernel launch for all t)
 //
 // enqueued without host synchronisation: termination (the reference's
 // decrease < eps rule, proj/src/solver.cpp:138-143) is decided on the device
