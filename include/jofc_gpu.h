@@ -155,6 +155,10 @@ int jofc_peer_export(jofc_ctx* ctx, void* ipc_handle_out, void** slab_out);
 int jofc_peer_attach(jofc_ctx* ctx, int rank, int world, const void* handles);
 int jofc_peer_attach_pointers(jofc_ctx* ctx, int rank, int world, void* const* slabs);
 int jofc_peer_detach(jofc_ctx* ctx);
+/* Device address through which this context reaches rank q's slab (its own
+ * for q == rank; the CUDA IPC mapping otherwise; NULL when not attached or
+ * attached by pointers).  Diagnostics. */
+void* jofc_peer_address(jofc_ctx* ctx, int q);
 /* Test driver: one solve over `world` peer-attached contexts of ONE process,
  * launched stage by stage with stream-event ordering so that no kernel ever
  * waits for a flag another context has not raised yet (a single GPU can host

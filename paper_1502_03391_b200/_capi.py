@@ -86,6 +86,7 @@ _SIGS = {
     "jofc_peer_attach": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
     "jofc_peer_attach_pointers": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
     "jofc_peer_detach": (C.c_int, [_vp]),
+    "jofc_peer_address": (_vp, [_vp, C.c_int]),
     "jofc_peer_lockstep_solve": (C.c_int, [C.POINTER(_vp), C.c_int, C.POINTER(Weights), _sz, _dp,
                                            C.c_double, _sz]),
     "jofc_oos_stress": (C.c_int, [_vp, _sz, _sz, _sz, _dp, _dp, _dp, C.c_double, _dp]),

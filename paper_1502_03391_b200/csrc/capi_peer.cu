@@ -227,6 +227,14 @@ int jofc_peer_attach_pointers(jofc_ctx* c, int rank, int world, void* const* sla
   return attach_common(c, rank, world, bases);
 }
 
+void* jofc_peer_address(jofc_ctx* c, int q) {
+  if (!c || !c->peer.active || q < 0 || q >= c->peer.world) return nullptr;
+  if (q == c->peer.rank) return c->peer.slab;
+  // the opened mappings are stored in rank order without this rank's own slab
+  const int idx = q < c->peer.rank ? q : q - 1;
+  return idx < static_cast<int>(c->peer.opened.size()) ? c->peer.opened[idx] : nullptr;
+}
+
 int jofc_peer_detach(jofc_ctx* c) {
   if (!c) return set_error(JOFC_EINVAL, "null context");
   JOFC_CUDA(cudaSetDevice(c->device));

@@ -130,3 +130,49 @@ def test_peer_missing_rank_fails_loudly():
                           init_config=wl.x0())
     with pytest.raises(jg.CommError, match="did not arrive"):
         jg.fjofc_embed(prob, wl.spec, opt, device=devs[0])
+
+
+def _ipc_worker(rank, world, port, out):
+    # the production attach path: slabs exported as CUDA IPC handles, handles
+    # all-gathered over torch.distributed (gloo), the other rank's slab opened;
+    # each rank then writes a marker into its own slab and reads the other's
+    # through its mapping (plain copies: no kernel waits on another)
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1502_03391_b200.dist import attach_peers, cuda_view
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    wl = workloads.make(1, n=200)
+    dev = jg.Device(0, shard=(rank, world))
+    dev.upload(jg.OmnibusProblem(list(wl.dense_delta()), validate=False))
+    handles = attach_peers(dev)
+    assert len(handles) == world and all(len(h) == 64 for h in handles)
+    own = dev.lib.jofc_peer_address(dev.h, rank)
+    other = dev.lib.jofc_peer_address(dev.h, 1 - rank)
+    assert own and other and own != other
+    cuda_view(own, 8, "cuda:0").copy_(
+        torch.full((8,), 1.5 * (rank + 1), dtype=torch.float64, device="cuda:0"))
+    torch.cuda.synchronize()
+    dist.barrier()
+    out[rank] = cuda_view(other, 8, "cuda:0").cpu().numpy().tolist()
+    dist.barrier()
+    dev.close()
+    dist.destroy_process_group()
+
+
+def test_peer_ipc_attach_two_processes():
+    import os
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ipc_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0] == [3.0] * 8 and out[1] == [1.5] * 8, dict(out)
