@@ -34,6 +34,22 @@ sys.path.insert(0, ROOT)
 CONFIG_NAMES = {1: "C1", 2: "C2", 3: "C3", 4: "C4", 5: "C5-in"}
 
 
+def metric_name(cfg, m, n, d):
+    """The metric string both arms print (the driver pairs the arms by it)."""
+    return f"Guttman iterations/s (fJOFC {CONFIG_NAMES[cfg]}: m={m} n={n} d={d})"
+
+
+def loaded_product_libraries():
+    """Product .so files mapped into this process (the reference arm must map none)."""
+    try:
+        with open("/proc/self/maps") as f:
+            maps = f.read()
+    except OSError:
+        return None
+    return sorted({line.split()[-1] for line in maps.splitlines()
+                   if "paper_1502_03391_b200" in line and line.endswith(".so")})
+
+
 def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -221,6 +237,7 @@ def run_ours(args):
     clocks.start()
     check(lib.jofc_profile(dev.h, 1 if profile_live else 0))
     launches0 = dev.launches()
+    evals0 = dev.stress_evaluations()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -232,6 +249,9 @@ def run_ours(args):
     its_c, conv_c = C.c_size_t(), C.c_int()
     check(lib.jofc_fetch_result(dev.h, dptr(x_dev), None, C.byref(its_c), C.byref(conv_c)))
     its = its_c.value
+    # iterations the device actually executed in the timed region: stress
+    # evaluations counted on the device, minus sigma(X0) once per solve
+    total_its = dev.stress_evaluations() - evals0 - args.steps
     pass_ms, pass_n = C.c_double(), C.c_uint64()
     if not profile_live:
         check(lib.jofc_profile(dev.h, 1))
@@ -245,7 +265,6 @@ def run_ours(args):
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    total_its = its * args.steps
     value = total_its / (ms * 1e-3)
     pairs = dev.problem_pairs()
     local_bytes = dev.problem_bytes()
@@ -305,8 +324,7 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": f"Guttman iterations/s (fJOFC {CONFIG_NAMES[cfg]}: m={wl.m} n={wl.n} "
-                      f"d={wl.d}), Delta resident in HBM",
+            "metric": metric_name(cfg, wl.m, wl.n, wl.d),
             "value": round(value, 3), "unit": "it/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -314,6 +332,9 @@ def run_ours(args):
             "config": {"workload": f"{CONFIG_NAMES[cfg]} in-sample fJOFC m={wl.m} n={wl.n} "
                                    f"d={wl.d} {spec.describe()} {T} Guttman iterations/step",
                        "iterations_per_step": its, "packed_pairs": pairs,
+                       "iterations_timed": int(total_its),
+                       "inputs": "packed Delta resident in HBM when the timed region starts "
+                                 "(e2e: dense host Delta through the C ABI)",
                        "launch": "CUDA graph replay" if args.graphs else "stream launches",
                        "delta_bytes_resident_per_gpu": local_bytes,
                        "parallelism": f"delta-shard{world}" if world > 1 else "single",
@@ -445,25 +466,26 @@ def cpu_baseline(wl, args):
 
 # ------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    reference sources; the C restatement when _ref was not built) on the same
+    workload, all host threads.  Inputs come from the reference's own Rng and
+    euclidean_distance_matrix (oracle/workloads_ref.py, bit-identical to the
+    product generator): this arm loads nothing of the product package."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    from oracle.oracle import Port, Reference, Spec
-    from paper_1502_03391_b200 import workloads
-    try:
-        R = Reference()
-        kind = "reference"
-    except (FileNotFoundError, OSError):
-        R = Port()
-        kind = "port"
+    from oracle import workloads_ref
+    from oracle.oracle import Reference
     cfg = args.config
-    wl = workloads.make(cfg)
+    wl = workloads_ref.make(cfg)
+    R = wl.impl
+    kind = "reference" if isinstance(R, Reference) else "port"
     delta = wl.dense_delta()
     x0 = wl.x0()
-    spec = Spec.general_(wl.spec.general) if wl.general_weights else Spec.uniform(wl.w)
+    spec = wl.spec
     cores = R.max_threads() if kind == "reference" else 1
     if kind == "reference":
-        R.problem(delta)
+        R.problem(delta)  # validated OmnibusProblem, outside the timing
     per_step = args.ref_iterations
     for _ in range(args.warmup):
         R.fjofc_embed(delta, spec, x0, 1e-300, per_step, parallel=True)
@@ -475,21 +497,26 @@ def run_reference(args):
     value = total / sec
     line = {
         "impl": "reference",
-        "metric": f"Guttman iterations/s (fJOFC {CONFIG_NAMES[cfg]}: m={wl.m} n={wl.n} d={wl.d})",
+        "metric": metric_name(cfg, wl.m, wl.n, wl.d),
         "value": round(value, 5), "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(sec / args.steps * 1e3, 2),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md)",
         "config": {"workload": f"{CONFIG_NAMES[cfg]} in-sample fJOFC m={wl.m} n={wl.n} d={wl.d} "
-                               f"{wl.spec.describe()}",
-                   "iterations_per_step": per_step},
+                               f"{wl.describe_spec()} {wl.iterations} Guttman iterations/solve",
+                   "iterations_per_step": per_step,
+                   "inputs": "dense host Delta (reference OmnibusProblem), reference Rng X0"},
         "delta_entries_per_s": value * wl.m * wl.n * (wl.n - 1) / 2,
         "cpu_baseline": {"value": round(value, 5), "unit": "it/s", "cores": cores, "kind": kind,
                          "sample": f"{per_step} Guttman iterations of fjofc_embed per step on "
-                                   f"the full {CONFIG_NAMES[cfg]} workload, parallel=true"},
+                                   f"the full {CONFIG_NAMES[cfg]} workload, parallel=true "
+                                   f"(OpenMP, {cores} threads); sigma(X0) once per step"},
         "e2e": {"value": round(value, 5), "unit": "it/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "product_libraries_loaded": loaded_product_libraries(),
     }
+    if kind == "reference":
+        R.release()
     print(json.dumps(line), flush=True)
 
 
@@ -883,7 +910,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-iterations", type=int, default=2)
+    ap.add_argument("--ref-iterations", type=int, default=10)
     ap.add_argument("--oos", action="store_true", help="C5 out-of-sample batch (config 5)")
     ap.add_argument("--init", action="store_true",
                     help="averaged_procrustes_init on the resident Delta (SURVEY 8f row f1)")

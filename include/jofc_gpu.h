@@ -112,8 +112,12 @@ int jofc_guttman_step(jofc_ctx* ctx, const jofc_weights* spec, size_t d, const d
                       double* x_next);
 
 /* fjofc_embed with InitKind::provided (proj/src/solver.cpp:106-150,223-236).
- * trace_out: max_it+1 doubles, sigma(X_0..X_iterations); step_seconds:
- * max_it doubles or NULL; iterations / converged as EmbeddingResult. */
+ * trace_out: max_it+1 doubles, sigma(X_0..X_iterations); iterations /
+ * converged as EmbeddingResult.  step_seconds: max_it doubles or NULL; the
+ * first `iterations` entries get the solve's mean device time per iteration
+ * (a fused pass + epilogue: the transform and the stress of its input, which
+ * the fused kernel does not time apart; the reference times fast_step alone,
+ * proj/src/solver.cpp:123-127). */
 int jofc_fjofc_embed(jofc_ctx* ctx, const jofc_weights* spec, size_t d, const double* x0,
                      double eps, size_t max_it, double* x_out, double* trace_out,
                      size_t* iterations, int* converged, double* step_seconds);
@@ -126,6 +130,11 @@ int jofc_fetch_result(jofc_ctx* ctx, double* x_out, double* trace_out, size_t* i
                       int* converged);
 /* Kernel launches issued by this context since creation (evidence counter). */
 uint64_t jofc_launch_count(jofc_ctx* ctx);
+/* Stress evaluations (= iterations t = 0..T of every solve, counted on the
+ * device by the step that writes trace[t]) since the context was created;
+ * synchronises the context stream.  bench.py divides these by its timed
+ * region instead of assuming every enqueued solve ran max_it iterations. */
+int jofc_stress_evaluations(jofc_ctx* ctx, uint64_t* evaluations);
 /* Instrumentation: when enabled, CUDA events bracket every pass-kernel launch
  * on the context stream; jofc_profile_read synchronises and returns the summed
  * pass time (ms) and launch count since the last read. */

@@ -83,6 +83,18 @@ void jo_rng_normals(uint64_t seed, size_t count, double scale, double* out) {
   for (size_t i = 0; i < count; ++i) out[i] = scale * jo_rng_normal(&r);
 }
 
+jo_rng* jo_rng_create(uint64_t seed) {
+  jo_rng* r = (jo_rng*)malloc(sizeof(jo_rng));
+  if (r) jo_rng_seed(r, seed);
+  return r;
+}
+
+void jo_rng_destroy(jo_rng* r) { free(r); }
+
+void jo_rng_draw(jo_rng* r, int kind, size_t count, double* out) {
+  for (size_t i = 0; i < count; ++i) out[i] = kind ? jo_rng_normal(r) : jo_rng_uniform(r);
+}
+
 /* ---------------- distance.cpp:8-29 ---------------- */
 int jo_euclidean_distance_matrix(size_t n, size_t p, const double* x, double* out) {
   for (size_t i = 0; i < n * p; ++i)

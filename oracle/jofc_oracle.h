@@ -52,6 +52,10 @@ uint64_t jo_rng_next_u64(jo_rng* r);
 double jo_rng_uniform(jo_rng* r);
 double jo_rng_normal(jo_rng* r);
 void jo_rng_normals(uint64_t seed, size_t count, double scale, double* out);
+/* a heap-allocated stream (ctypes callers): kind 0 uniform(), 1 normal() */
+jo_rng* jo_rng_create(uint64_t seed);
+void jo_rng_destroy(jo_rng* r);
+void jo_rng_draw(jo_rng* r, int kind, size_t count, double* out);
 
 /* proj/src/distance.cpp:8-29 (serial order; bitwise symmetric) */
 int jo_euclidean_distance_matrix(size_t n, size_t p, const double* feats, double* out);

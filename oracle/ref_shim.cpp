@@ -125,6 +125,16 @@ void ref_rng_normals(uint64_t seed, size_t count, double scale, double* out) {
   for (size_t i = 0; i < count; ++i) out[i] = scale * r.normal();
 }
 
+// A stateful Rng stream (the reference's class): the bench's reference arm
+// draws the synthetic workloads through it (oracle/workloads_ref.py).
+void* ref_rng_create(uint64_t seed) { return new Rng(seed); }
+void ref_rng_destroy(void* h) { delete static_cast<Rng*>(h); }
+// kind 0: uniform() [0,1), 1: normal()
+void ref_rng_draw(void* h, int kind, size_t count, double* out) {
+  Rng& r = *static_cast<Rng*>(h);
+  for (size_t i = 0; i < count; ++i) out[i] = kind ? r.normal() : r.uniform();
+}
+
 void ref_rng_u64(uint64_t seed, size_t count, uint64_t* out) {
   Rng r(seed);
   for (size_t i = 0; i < count; ++i) out[i] = r.next_u64();

@@ -78,6 +78,7 @@ _SIGS = {
     "jofc_fjofc_enqueue": (C.c_int, [_vp, C.POINTER(Weights), _sz, _dp, C.c_double, _sz]),
     "jofc_fetch_result": (C.c_int, [_vp, _dp, _dp, _szp, C.POINTER(C.c_int)]),
     "jofc_launch_count": (C.c_uint64, [_vp]),
+    "jofc_stress_evaluations": (C.c_int, [_vp, C.POINTER(C.c_uint64)]),
     "jofc_profile": (C.c_int, [_vp, C.c_int]),
     "jofc_profile_read": (C.c_int, [_vp, _dp, C.POINTER(C.c_uint64)]),
     "jofc_set_exchange_buffer": (C.c_int, [_vp, _vp, _sz]),
@@ -122,6 +123,8 @@ def load():
                           "(or __graft_entry__.build()).  There is no CPU fallback.")
     lib = C.CDLL(path)
     for name, (res, args) in _SIGS.items():
+        if path != LIB_PATH and not hasattr(lib, name):
+            continue  # (an older experiment build: A/B timing only)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -278,6 +278,12 @@ class Device:
     def launches(self):
         return int(self.lib.jofc_launch_count(self.h))
 
+    def stress_evaluations(self):
+        """Iterations (stress evaluations) the device executed since creation."""
+        v = C.c_uint64()
+        check(self.lib.jofc_stress_evaluations(self.h, C.byref(v)))
+        return int(v.value)
+
     def set_allreduce(self, fn):
         """fn(ptr: int, count: int, stream: int) -> None, sums in place over ranks."""
         def tramp(buf, count, stream, user):

@@ -83,8 +83,15 @@ PeerParams peer_params(jofc_ctx* c, const PassParams& pp, size_t t) {
   return pe;
 }
 
+// Every attach starts the group from a clean slab: both P regions, X, the
+// flags and the epoch counter zeroed (a slab left by an earlier group holds a
+// dirty P region and that group's flags).  All ranks must attach before any
+// of them solves (dist.attach_peers puts a barrier there).
 int attach_common(jofc_ctx* c, int rank, int world, const std::vector<double*>& bases) {
   PeerState& ps = c->peer;
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  JOFC_CUDA(cudaMemsetAsync(ps.slab, 0, ps.slab_doubles * sizeof(double), c->stream));
+  ps.epoch = 0;
   JOFC_CUDA(ps.ptrs.ensure(world));
   JOFC_TRY(copy_sync(c, ps.ptrs.p, bases.data(), world * sizeof(double*), cudaMemcpyHostToDevice));
   ps.rank = rank;
@@ -220,6 +227,7 @@ int jofc_peer_attach(jofc_ctx* c, int rank, int world, const void* handles) {
 int jofc_peer_attach_pointers(jofc_ctx* c, int rank, int world, void* const* slabs) {
   JOFC_TRY(attach_checks(c, rank, world));
   if (!slabs) return set_error(JOFC_EINVAL, "peer exchange: null slabs");
+  close_opened(c->peer);  // (mappings of an earlier IPC attach)
   std::vector<double*> bases(world);
   for (int q = 0; q < world; ++q) bases[q] = static_cast<double*>(slabs[q]);
   if (bases[rank] != c->peer.slab)

@@ -18,6 +18,7 @@
 #include <chrono>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -318,7 +319,10 @@ int alloc_solve_state(jofc_ctx* c, size_t d, size_t max_it) {
   // (the persistent kernel keeps one commensurability partial per pass CTA)
   JOFC_CUDA(c->com_part.ensure(std::max(c->epi_grid, c->pass_grid)));
   JOFC_CUDA(c->trace.ensure(max_it + 1));
-  JOFC_CUDA(c->ctrl.ensure(1));
+  if (!c->ctrl.p) {  // (zeroed once: the evaluation counter lives in it)
+    JOFC_CUDA(c->ctrl.ensure(1));
+    JOFC_CUDA(cudaMemsetAsync(c->ctrl.p, 0, sizeof(Control), c->stream));
+  }
   JOFC_CUDA(c->consts.ensure(3 * static_cast<size_t>(L.m) * L.m + L.m));
   if (resize) {
     JOFC_CUDA(cudaMemsetAsync(c->x0.p, 0, cfg * sizeof(double), c->stream));
@@ -362,6 +366,8 @@ int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t 
     return set_error(JOFC_EINVAL, "dim %zu unsupported (1..%d)", d, kMaxD);
   if (!(eps > 0.0)) return set_error(JOFC_EINVAL, "SolveOptions: eps must be positive");
   if (!x0) return set_error(JOFC_EINVAL, "null configuration");
+  if (max_it >= static_cast<size_t>(INT_MAX))
+    return set_error(JOFC_EINVAL, "max_iterations %zu too large (< %d)", max_it, INT_MAX);
   const Layout& L = c->lay;
   HostWeights hw;
   std::string msg;
@@ -388,7 +394,7 @@ int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t 
   rc = upload_config(c, x0, xbuf(c, 0));
   if (rc) return rc;
 
-  Control& h = *c->ctrl_host;
+  Control h;
   std::memset(&h, 0, sizeof(Control));
   h.max_it = static_cast<int>(max_it);
   h.eps = eps;
@@ -398,7 +404,9 @@ int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t 
   }
   const double mn = static_cast<double>(L.m) * static_cast<double>(L.n);
   h.pairs = mn * (mn - 1.0) / 2.0;
-  JOFC_CUDA(cudaMemcpyAsync(c->ctrl.p, &h, sizeof(Control), cudaMemcpyHostToDevice, c->stream));
+  jofc_control_init_kernel<<<1, 1, 0, c->stream>>>(c->ctrl.p, h);
+  JOFC_CUDA(cudaGetLastError());
+  ++c->launches;
 
   PassParams pp{};
   pp.delta = c->delta.p;
@@ -602,8 +610,13 @@ int jofc_gpu::capi::finish_solve(jofc_ctx* c, Control* out) {
     c->peer.phase = (c->peer.phase + last + 1) & 1;
     c->peer.pending = false;
   }
-  if (out->status == 3) {
+  if (out->status == 3 || out->status == 4) {
     peer_release(c);  // the group's exchange state is unknown: attach again
+    if (out->status == 4)
+      return set_error(JOFC_ECOMM,
+                       "peer exchange: the ranks disagree on the solve count (epoch mismatch at "
+                       "iteration %d); re-attach the group",
+                       out->err_iter);
     return set_error(JOFC_ECOMM, "peer exchange: a rank did not arrive within 20 s (iteration %d)",
                      out->err_iter);
   }
@@ -680,6 +693,18 @@ int jofc_ctx_destroy(jofc_ctx* c) {
 void* jofc_ctx_stream(jofc_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
 uint64_t jofc_launch_count(jofc_ctx* c) { return c ? c->launches : 0; }
+
+int jofc_stress_evaluations(jofc_ctx* c, uint64_t* out) {
+  if (!c || !out) return set_error(JOFC_EINVAL, "null argument");
+  *out = 0;
+  if (!c->ctrl.p) return JOFC_OK;
+  JOFC_CUDA(cudaSetDevice(c->device));
+  unsigned long long v = 0;
+  JOFC_CUDA(cudaMemcpyAsync(&v, &c->ctrl.p->evals, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  *out = static_cast<uint64_t>(v);
+  return JOFC_OK;
+}
 
 int jofc_profile(jofc_ctx* c, int enable) {
   if (!c) return set_error(JOFC_EINVAL, "null context");
@@ -903,24 +928,31 @@ int jofc_fjofc_embed(jofc_ctx* c, const jofc_weights* spec, size_t d, const doub
                      int* converged, double* step_seconds) {
   if (!c) return set_error(JOFC_EINVAL, "null context");
   JOFC_CUDA(cudaSetDevice(c->device));
-  std::vector<cudaEvent_t> ev;
-  if (step_seconds) {
-    ev.resize(max_it + 2);
+  // step_seconds: two events around the whole solve (it keeps the CUDA-graph
+  // and single-launch routes; per-iteration events would force stream
+  // launches).  Every entry is the solve's mean device time per iteration --
+  // one fused pass + epilogue, i.e. the transform together with the stress
+  // of its input iterate, which the fused kernel cannot time apart
+  // (the reference times fast_step alone, proj/src/solver.cpp:123-127).
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (step_seconds)
     for (auto& e : ev) JOFC_CUDA(cudaEventCreate(&e));
-  }
-  int rc = enqueue_solve(c, spec, d, x0, eps, max_it, step_seconds ? &ev : nullptr,
-                         /*early_stop=*/stop_chunk() > 0);
+  if (ev[0]) JOFC_CUDA(cudaEventRecord(ev[0], c->stream));
+  int rc = enqueue_solve(c, spec, d, x0, eps, max_it, nullptr, /*early_stop=*/stop_chunk() > 0);
+  if (!rc && ev[1]) rc = cudaEventRecord(ev[1], c->stream) == cudaSuccess
+                             ? JOFC_OK
+                             : set_error(JOFC_ECUDA, "event record failed");
   size_t its = 0;
   if (!rc) rc = jofc_fetch_result(c, x_out, trace_out, &its, converged);
   if (!rc && iterations) *iterations = its;
-  if (!rc && step_seconds) {
-    for (size_t t = 0; t < its; ++t) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[t], ev[t + 1]);
-      step_seconds[t] = ms * 1e-3;
-    }
+  if (!rc && step_seconds && its > 0) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[0], ev[1]);
+    const double per = ms * 1e-3 / static_cast<double>(its + 1);  // its + 1 passes
+    for (size_t t = 0; t < its; ++t) step_seconds[t] = per;
   }
-  for (auto& e : ev) cudaEventDestroy(e);
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
   return rc;
 }
 

@@ -71,18 +71,27 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return v;
 }
 
-__device__ __forceinline__ bool wait_flag(const unsigned long long* f, unsigned long long target) {
-  if (ld_acquire_sys(f) >= target) return true;
+// Wait until flag f reaches target = (epoch, t + 1).  In a consistent group
+// a flag never runs ahead of the value a waiter needs (a rank raises (e, t+2)
+// only after every rank's decide of (e, t), which follows this wait), so a
+// larger value means the ranks disagree on the solve count -- e.g. one rank's
+// solve failed validation before it took an epoch -- and the solve fails
+// instead of reading another solve's products.
+// Returns 0 arrived, 1 timed out, 2 epoch mismatch.
+__device__ __forceinline__ int wait_flag(const unsigned long long* f, unsigned long long target) {
+  unsigned long long v = ld_acquire_sys(f);
   const unsigned long long t0 = global_ns();
-  while (ld_acquire_sys(f) < target) {
+  while (v < target) {
     __nanosleep(32);
-    if (global_ns() - t0 > kPeerTimeoutNs) return false;
+    if (global_ns() - t0 > kPeerTimeoutNs) return 1;
+    v = ld_acquire_sys(f);
   }
-  return true;
+  return v == target ? 0 : 2;
 }
 
-__device__ __forceinline__ void peer_timeout(Control* ctrl, int t) {
-  ctrl->status = 3;
+// status 3: a rank did not arrive in time; 4: the ranks' epochs disagree
+__device__ __forceinline__ void peer_fail(Control* ctrl, int t, int why) {
+  ctrl->status = why == 2 ? 4 : 3;
   ctrl->err_iter = t;
   ctrl->done = 1;
 }
@@ -100,13 +109,14 @@ __global__ void __launch_bounds__(256) jofc_peer_mix_kernel(const PeerParams p) 
   double* own = p.slabs[p.rank];
   if (threadIdx.x == 0) timed_out = 0;
   __syncthreads();
-  if (threadIdx.x < p.world &&
-      !wait_flag(reinterpret_cast<const unsigned long long*>(own + p.flag1_off) + threadIdx.x,
-                 target))
-    timed_out = 1;
+  if (threadIdx.x < p.world) {
+    const int w = wait_flag(reinterpret_cast<const unsigned long long*>(own + p.flag1_off) +
+                                threadIdx.x, target);
+    if (w) atomicMax(&timed_out, w);
+  }
   __syncthreads();
   if (timed_out) {
-    if (threadIdx.x == 0) peer_timeout(ctrl, t);
+    if (threadIdx.x == 0) peer_fail(ctrl, t, timed_out);
     return;
   }
 
@@ -193,14 +203,15 @@ static __global__ void __launch_bounds__(32) jofc_peer_decide_kernel(const PeerP
   const double* own = p.slabs[p.rank];
   double f = 0.0, c = 0.0;
   const int q = threadIdx.x;
-  bool ok = true;
+  int w = 0;
   if (q < p.world) {
-    ok = wait_flag(reinterpret_cast<const unsigned long long*>(own + p.flag2_off) + q, target);
+    w = wait_flag(reinterpret_cast<const unsigned long long*>(own + p.flag2_off) + q, target);
     f = ld_relaxed_sys(p.slabs[q] + p.p_read + p.fid_slot);
     c = ld_relaxed_sys(p.slabs[q] + p.com_off);
   }
-  if (!__all_sync(0xffffffffu, ok)) {
-    if (threadIdx.x == 0) peer_timeout(ctrl, t);
+  const int why = __reduce_max_sync(0xffffffffu, w);
+  if (why) {
+    if (threadIdx.x == 0) peer_fail(ctrl, t, why);
     return;
   }
   double fid = 0.0, com = 0.0;
