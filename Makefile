@@ -12,7 +12,7 @@ CSRC    := $(PKG)/csrc
 NVFLAGS := $(EXTRA) -O3 -std=c++17 $(ARCH) -lineinfo -Iinclude -I$(CSRC) \
            -Xcompiler -fPIC,-fopenmp,-Wall -ccbin $(CXX)
 GPU_SRC := $(CSRC)/jofc_capi.cu $(CSRC)/capi_init.cu $(CSRC)/capi_ingest.cu $(CSRC)/capi_peer.cu \
-           $(CSRC)/jofc_weights.cpp $(CSRC)/workloads.cpp $(CSRC)/ingest_io.cpp
+           $(CSRC)/jofc_weights.cpp $(CSRC)/host_linalg.cpp $(CSRC)/workloads.cpp $(CSRC)/ingest_io.cpp
 GPU_HDR := $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/jofc_gpu.h include/jofc_workloads.h
 DROPIN_SRC := $(wildcard $(CSRC)/dropin/*.cpp)
 DROPIN_HDR := $(wildcard include/jofc/*.hpp)

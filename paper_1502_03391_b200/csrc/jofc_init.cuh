@@ -11,13 +11,14 @@
 // runs with its n x p panels resident: S Q as a bandwidth-bound tiled kernel,
 // the Ritz/Gram products and the re-orthogonalisation as O(n p^2) kernels.
 // Same start (Rng(0x9e3779b97f4a7c15) normals, Gram-Schmidt on the host), same
-// cyclic Jacobi on the p x p Ritz matrix (host), same stopping residual
-// 1e-9 ||S||_F.  The reference re-orthogonalises with Gram-Schmidt plus one
+// cyclic Jacobi on the p x p Ritz matrix (host, host_linalg.h), same
+// stopping residual 1e-9 ||S||_F.  The reference re-orthogonalises with Gram-Schmidt plus one
 // re-orthogonalisation; here it is Cholesky-QR twice (same Q in exact
 // arithmetic, rounding-level difference), falling back to host Gram-Schmidt
 // when the panel is too ill-conditioned for Cholesky.  For n <= 320 the
-// reference's full cyclic Jacobi on the whole S runs on the host; the d x d
-// Procrustes rotation uses its one-sided Jacobi SVD (proj/src/linalg.cpp:333-416).
+// reference's route -- cyclic Jacobi on the whole S -- runs on the host; the
+// d x d Procrustes rotation comes from a one-sided Jacobi SVD (the shared
+// host_linalg.h routines, proj/src/linalg.cpp's contracts).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -29,7 +30,9 @@
 #include <stdexcept>
 #include <vector>
 
+#include "host_linalg.h"
 #include "jofc_layout.h"
+#include "jofc_rng.h"
 
 namespace jofc_gpu {
 namespace init {
@@ -412,200 +415,32 @@ struct Mat {
   double operator()(std::size_t i, std::size_t j) const { return a[i * c + j]; }
 };
 
-// The reference Rng's normal stream (mt19937_64, 53-bit uniforms, Box-Muller
-// with cached sine) -- proj/include/jofc/rng.hpp:17-55.
+// The start panel's normal stream: the reference's Rng (jofc_rng.h).
 class Normals {
  public:
-  explicit Normals(uint64_t seed) : e_(seed) {}
-  double next() {
-    if (have_) {
-      have_ = false;
-      return spare_;
-    }
-    double u1 = uni();
-    while (u1 <= 0.0) u1 = uni();
-    const double u2 = uni();
-    const double rad = std::sqrt(-2.0 * std::log(u1));
-    const double th = 2.0 * 3.14159265358979323846 * u2;
-    spare_ = rad * std::sin(th);
-    have_ = true;
-    return rad * std::cos(th);
-  }
+  explicit Normals(uint64_t seed) : rng_(seed) {}
+  double next() { return rng_.normal(); }
 
  private:
-  double uni() { return static_cast<double>(e_() >> 11) * 0x1.0p-53; }
-  std::mt19937_64 e_;
-  double spare_ = 0.0;
-  bool have_ = false;
+  RefRng rng_;
 };
 
-// Cyclic Jacobi eigen-decomposition (rotation by rotation as the reference's
-// jacobi_decompose, sweep cap 100, off-diagonal tolerance 1e-12 ||A||_F).
-inline bool jacobi_eigen(Mat a, std::vector<double>& values, Mat& v) {
-  const std::size_t n = a.r;
-  v = Mat(n, n);
-  for (std::size_t i = 0; i < n; ++i) v(i, i) = 1.0;
-  double fro = 0.0;
-  for (double x : a.a) fro += x * x;
-  const double tol = 1e-12 * std::sqrt(fro);
-  auto off = [&]() {
-    double s = 0.0;
-    for (std::size_t i = 0; i < n; ++i)
-      for (std::size_t j = i + 1; j < n; ++j) s += 2.0 * a(i, j) * a(i, j);
-    return std::sqrt(s);
-  };
-  int sweep = 0;
-  for (; sweep < 100; ++sweep) {
-    if (off() <= tol) break;
-    for (std::size_t p = 0; p + 1 < n; ++p)
-      for (std::size_t q = p + 1; q < n; ++q) {
-        const double apq = a(p, q);
-        if (apq == 0.0) continue;
-        const double tau = (a(q, q) - a(p, p)) / (2.0 * apq);
-        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (std::abs(tau) + std::sqrt(1.0 + tau * tau));
-        const double cs = 1.0 / std::sqrt(1.0 + t * t);
-        const double sn = t * cs;
-        const double app = a(p, p), aqq = a(q, q);
-        a(p, p) = app - t * apq;
-        a(q, q) = aqq + t * apq;
-        a(p, q) = a(q, p) = 0.0;
-        for (std::size_t r = 0; r < n; ++r) {
-          if (r == p || r == q) continue;
-          const double arp = a(r, p), arq = a(r, q);
-          a(r, p) = a(p, r) = cs * arp - sn * arq;
-          a(r, q) = a(q, r) = sn * arp + cs * arq;
-        }
-        for (std::size_t r = 0; r < n; ++r) {
-          const double vrp = v(r, p), vrq = v(r, q);
-          v(r, p) = cs * vrp - sn * vrq;
-          v(r, q) = sn * vrp + cs * vrq;
-        }
-      }
-  }
-  if (sweep == 100 && off() > tol) return false;
-  values.resize(n);
-  for (std::size_t i = 0; i < n; ++i) values[i] = a(i, i);
-  return true;
+// Host algebra on Mat: the shared routines of host_linalg.h.
+inline bool jacobi_eigen(const Mat& a, std::vector<double>& values, Mat& v) {
+  values.resize(a.r);
+  v = Mat(a.r, a.r);
+  return hostla::jacobi_eigh(a.a.data(), a.r, values.data(), v.a.data());
 }
 
-// Largest-magnitude component made positive (the reference's sign convention).
-inline void fix_sign(std::vector<double>& vec) {
-  std::size_t arg = 0;
-  double best = 0.0;
-  for (std::size_t i = 0; i < vec.size(); ++i)
-    if (std::abs(vec[i]) > best) {
-      best = std::abs(vec[i]);
-      arg = i;
-    }
-  if (!vec.empty() && vec[arg] < 0.0)
-    for (double& x : vec) x = -x;
-}
+inline void fix_sign(std::vector<double>& vec) { hostla::orient(vec.data(), vec.size()); }
 
-// Gram-Schmidt of column j against columns < j, twice (re-orthogonalisation).
-inline void project_out(Mat& q, std::size_t j) {
-  for (int pass = 0; pass < 2; ++pass)
-    for (std::size_t i = 0; i < j; ++i) {
-      double dot = 0.0;
-      for (std::size_t r = 0; r < q.r; ++r) dot += q(r, i) * q(r, j);
-      for (std::size_t r = 0; r < q.r; ++r) q(r, j) -= dot * q(r, i);
-    }
-}
+inline void orthonormalize(Mat& q) { hostla::orthonormalize_columns(q.a.data(), q.r, q.c); }
 
-inline void orthonormalize(Mat& q) {
-  for (std::size_t j = 0; j < q.c; ++j) {
-    project_out(q, j);
-    double nrm = 0.0;
-    for (std::size_t r = 0; r < q.r; ++r) nrm += q(r, j) * q(r, j);
-    nrm = std::sqrt(nrm);
-    if (nrm < 1e-150) {  // vanished column: first coordinate vector outside the span
-      for (std::size_t e = 0; e < q.r; ++e) {
-        for (std::size_t r = 0; r < q.r; ++r) q(r, j) = (r == e) ? 1.0 : 0.0;
-        project_out(q, j);
-        double n2 = 0.0;
-        for (std::size_t r = 0; r < q.r; ++r) n2 += q(r, j) * q(r, j);
-        n2 = std::sqrt(n2);
-        if (n2 > 1e-8) {
-          nrm = n2;
-          break;
-        }
-      }
-    }
-    for (std::size_t r = 0; r < q.r; ++r) q(r, j) /= nrm;
-  }
-}
-
-// One-sided Jacobi SVD of a small square matrix -> (U, V) with the reference's
-// ordering and deterministic completion of U (proj/src/linalg.cpp:333-416).
-inline void svd_small(const Mat& a, Mat& u, Mat& vout) {
-  const std::size_t n = a.r;
-  Mat g = a, v(n, n);
-  for (std::size_t i = 0; i < n; ++i) v(i, i) = 1.0;
-  for (int sweep = 0; sweep < 64; ++sweep) {
-    bool rotated = false;
-    for (std::size_t p = 0; p + 1 < n; ++p)
-      for (std::size_t q = p + 1; q < n; ++q) {
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (std::size_t r = 0; r < n; ++r) {
-          al += g(r, p) * g(r, p);
-          be += g(r, q) * g(r, q);
-          ga += g(r, p) * g(r, q);
-        }
-        if (std::abs(ga) <= 1e-14 * std::sqrt(al * be) || ga == 0.0) continue;
-        rotated = true;
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / std::sqrt(1.0 + t * t);
-        const double sn = cs * t;
-        for (std::size_t r = 0; r < n; ++r) {
-          const double gp = g(r, p), gq = g(r, q);
-          g(r, p) = cs * gp - sn * gq;
-          g(r, q) = sn * gp + cs * gq;
-          const double vp = v(r, p), vq = v(r, q);
-          v(r, p) = cs * vp - sn * vq;
-          v(r, q) = sn * vp + cs * vq;
-        }
-      }
-    if (!rotated) break;
-  }
-  std::vector<double> sig(n);
-  for (std::size_t j = 0; j < n; ++j) {
-    double nr = 0.0;
-    for (std::size_t r = 0; r < n; ++r) nr += g(r, j) * g(r, j);
-    sig[j] = std::sqrt(nr);
-  }
-  std::vector<std::size_t> order(n);
-  std::iota(order.begin(), order.end(), std::size_t{0});
-  std::stable_sort(order.begin(), order.end(),
-                   [&](std::size_t x, std::size_t y) { return sig[x] > sig[y]; });
-  u = Mat(n, n);
-  vout = Mat(n, n);
-  const double rank_tol = 1e-13 * std::max(1.0, n ? sig[order[0]] : 0.0);
-  std::size_t filled = 0;
-  for (std::size_t j = 0; j < n; ++j) {
-    const std::size_t src = order[j];
-    for (std::size_t r = 0; r < n; ++r) vout(r, j) = v(r, src);
-    if (sig[src] > rank_tol) {
-      for (std::size_t r = 0; r < n; ++r) u(r, j) = g(r, src) / sig[src];
-      filled = j + 1;
-    }
-  }
-  for (std::size_t j = filled; j < n; ++j)
-    for (std::size_t e = 0; e < n; ++e) {
-      std::vector<double> cand(n, 0.0);
-      cand[e] = 1.0;
-      for (std::size_t i = 0; i < j; ++i) {
-        double dot = 0.0;
-        for (std::size_t r = 0; r < n; ++r) dot += u(r, i) * cand[r];
-        for (std::size_t r = 0; r < n; ++r) cand[r] -= dot * u(r, i);
-      }
-      double nr = 0.0;
-      for (double x : cand) nr += x * x;
-      nr = std::sqrt(nr);
-      if (nr > 1e-6) {
-        for (std::size_t r = 0; r < n; ++r) u(r, j) = cand[r] / nr;
-        break;
-      }
-    }
+inline void svd_small(const Mat& a, Mat& u, Mat& v) {
+  u = Mat(a.r, a.r);
+  v = Mat(a.r, a.r);
+  std::vector<double> sig(a.r);
+  hostla::svd_jacobi(a.a.data(), a.r, u.a.data(), sig.data(), v.a.data());
 }
 
 inline void center_columns(Mat& x) {

@@ -1,6 +1,8 @@
 // jofc_weights.cpp -- see jofc_weights.h.
 #include "jofc_weights.h"
 
+#include "host_linalg.h"
+
 #include <algorithm>
 #include <cmath>
 
@@ -24,41 +26,6 @@ double cross_of(const jofc_weights* s, std::size_t m, std::size_t i, std::size_t
     case 2: return s->within[i] * s->within[j];
     default: return s->w;
   }
-}
-
-// Partial-pivot Gauss-Jordan (proj/src/linalg.cpp:296-331 semantics).
-bool gauss_jordan(std::size_t n, std::vector<double> a, std::vector<double>& inv) {
-  double amax = 0.0;
-  for (double v : a) amax = std::max(amax, std::fabs(v));
-  const double floor_v = 1e-13 * std::max(1.0, amax);
-  inv.assign(n * n, 0.0);
-  for (std::size_t i = 0; i < n; ++i) inv[i * n + i] = 1.0;
-  for (std::size_t col = 0; col < n; ++col) {
-    std::size_t piv = col;
-    for (std::size_t r = col + 1; r < n; ++r)
-      if (std::fabs(a[r * n + col]) > std::fabs(a[piv * n + col])) piv = r;
-    if (std::fabs(a[piv * n + col]) < floor_v) return false;
-    if (piv != col)
-      for (std::size_t j = 0; j < n; ++j) {
-        std::swap(a[piv * n + j], a[col * n + j]);
-        std::swap(inv[piv * n + j], inv[col * n + j]);
-      }
-    const double dv = a[col * n + col];
-    for (std::size_t j = 0; j < n; ++j) {
-      a[col * n + j] /= dv;
-      inv[col * n + j] /= dv;
-    }
-    for (std::size_t r = 0; r < n; ++r) {
-      if (r == col) continue;
-      const double f = a[r * n + col];
-      if (f == 0.0) continue;
-      for (std::size_t j = 0; j < n; ++j) {
-        a[r * n + j] -= f * a[col * n + j];
-        inv[r * n + j] -= f * inv[col * n + j];
-      }
-    }
-  }
-  return true;
 }
 
 }  // namespace
@@ -156,7 +123,7 @@ int build_weights(const jofc_weights* s, std::size_t m, std::size_t n, HostWeigh
     for (std::size_t i = 0; i < m; ++i)
       for (std::size_t j = 0; j < m; ++j)
         inv[i * m + j] = (i == j) ? 1.0 / (s->within[i] * (cn + sum)) + off : off;
-  } else if (!gauss_jordan(m, W, inv)) {
+  } else if (!hostla::gauss_jordan_inverse(W.data(), m, inv.data())) {
     *msg = "invert_small: singular matrix";
     return JOFC_ENUMERIC;
   }

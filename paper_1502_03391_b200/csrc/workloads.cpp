@@ -2,6 +2,8 @@
 // See include/jofc_workloads.h and DESIGN.md "Synthetic workloads".
 #include "jofc_workloads.h"
 
+#include "jofc_rng.h"
+
 #include <cmath>
 #include <cstring>
 #include <random>
@@ -9,33 +11,7 @@
 
 namespace {
 
-// The reference's Rng arithmetic (proj/include/jofc/rng.hpp:17-55) on
-// std::mt19937_64, whose output sequence the C++ standard fixes.
-class Rng {
- public:
-  explicit Rng(uint64_t seed) : e_(seed) {}
-  double uniform() { return static_cast<double>(e_() >> 11) * 0x1.0p-53; }
-  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
-  double normal() {
-    if (have_) {
-      have_ = false;
-      return spare_;
-    }
-    double u1 = uniform();
-    while (u1 <= 0.0) u1 = uniform();
-    const double u2 = uniform();
-    const double r = std::sqrt(-2.0 * std::log(u1));
-    const double th = 2.0 * 3.14159265358979323846 * u2;
-    spare_ = r * std::sin(th);
-    have_ = true;
-    return r * std::cos(th);
-  }
-
- private:
-  std::mt19937_64 e_;
-  double spare_ = 0.0;
-  bool have_ = false;
-};
+using Rng = jofc_gpu::RefRng;
 
 // Gram-Schmidt on a Gaussian draw, column by column.
 std::vector<double> random_orthogonal(Rng& rng, size_t q) {
