@@ -12,6 +12,7 @@ CSRC    := $(PKG)/csrc
 NVFLAGS := $(EXTRA) -O3 -std=c++17 $(ARCH) -lineinfo -Iinclude -I$(CSRC) \
            -Xcompiler -fPIC,-fopenmp,-Wall -ccbin $(CXX)
 GPU_SRC := $(CSRC)/jofc_capi.cu $(CSRC)/capi_init.cu $(CSRC)/capi_ingest.cu $(CSRC)/capi_peer.cu \
+           $(CSRC)/capi_nccl.cu \
            $(CSRC)/jofc_weights.cpp $(CSRC)/host_linalg.cpp $(CSRC)/workloads.cpp $(CSRC)/ingest_io.cpp
 GPU_HDR := $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/jofc_gpu.h include/jofc_workloads.h
 DROPIN_SRC := $(wildcard $(CSRC)/dropin/*.cpp)
@@ -24,12 +25,12 @@ $(PKG)/libjofc_probe.so: $(CSRC)/probe.cu
 	$(NVCC) $(NVFLAGS) -shared -o $@ $<
 
 $(PKG)/libjofc_gpu.so: $(GPU_SRC) $(GPU_HDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPU_SRC) -lgomp
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPU_SRC) -lgomp -ldl
 
 # kernel experiments: `make exp EXP=-DJOFC_EXP_...` builds the same C ABI with an
 # experimental switch into libjofc_gpu_exp.so (selected with JOFC_GPU_LIB)
 exp:
-	$(NVCC) $(NVFLAGS) $(EXP) -shared -o $(PKG)/libjofc_gpu_exp.so $(GPU_SRC) -lgomp
+	$(NVCC) $(NVFLAGS) $(EXP) -shared -o $(PKG)/libjofc_gpu_exp.so $(GPU_SRC) -lgomp -ldl
 
 $(PKG)/libjofc.so: $(DROPIN_SRC) $(DROPIN_HDR) $(PKG)/libjofc_gpu.so
 	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -I$(CSRC) -o $@ $(DROPIN_SRC) \

@@ -202,9 +202,13 @@ def run_ours(args):
         # loop's own kernels (csrc/jofc_peer.cuh), slabs mapped by CUDA IPC
         from paper_1502_03391_b200.dist import attach_peers
         attach_peers(dev)
-    elif world > 1:
+    elif world > 1 and args.exchange == "hook":
         from paper_1502_03391_b200.dist import attach_nccl
         attach_nccl(dev, wl.d)  # torch-owned exchange buffer, NCCL all-reduce on dev.stream
+    elif world > 1:
+        # the C ABI's own NCCL reduce-scatter + all-gather, in the CUDA graph
+        from paper_1502_03391_b200.dist import attach_nccl_native
+        attach_nccl_native(dev)
 
     import ctypes as C
     eps, T = 1e-300, wl.iterations
@@ -342,7 +346,11 @@ def run_ours(args):
                                       "peer memory: reduce-scatter read + mix + all-gather "
                                       "write in the loop's kernels (NVLink loads/stores)"
                                       if args.exchange == "peer" else
-                                      f"{backend} all-reduce of P + fidelity per iteration"),
+                                      f"{backend} all-reduce of P + fidelity per iteration "
+                                      f"(Python hook)" if args.exchange == "hook" else
+                                      "C-ABI NCCL per iteration: m x reduce-scatter of P row "
+                                      "chunks + all-reduce of the fidelity, own-row mix, "
+                                      "m x all-gather of X rows; in the CUDA graph"),
                        "l2": "inputs larger than L2 (packed Delta %.2f GB vs 126 MB L2)" % (local_bytes / 1e9)
                        if local_bytes > 126e6 * 4 else "Delta may be L2-resident"},
             "delta_entries_per_s": value * pairs,
@@ -917,8 +925,9 @@ def main():
     ap.add_argument("--ingest", action="store_true",
                     help="stream a .jofc problem file into the device layout (SURVEY 8f row f2)")
     ap.add_argument("--exchange", default=os.environ.get("JOFC_EXCHANGE", "nccl"),
-                    choices=["nccl", "peer"],
-                    help="multi-GPU exchange: NCCL all-reduce hook or peer-memory kernels")
+                    choices=["nccl", "hook", "peer"],
+                    help="multi-GPU exchange: the C ABI's NCCL reduce-scatter/all-gather "
+                         "(default), a Python all-reduce hook, or peer-memory kernels")
     ap.add_argument("--graphs", type=int, default=None,
                     help="replay CUDA graphs in the timed region (default: on for configs 1,2,5)")
     args = ap.parse_args()

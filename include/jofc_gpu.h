@@ -146,6 +146,24 @@ int jofc_profile_read(jofc_ctx* ctx, double* pass_ms, uint64_t* pass_launches);
 int jofc_set_exchange_buffer(jofc_ctx* ctx, double* device_buf, size_t capacity);
 size_t jofc_exchange_count(jofc_ctx* ctx, size_t d);
 
+/* C-native NCCL exchange (csrc/capi_nccl.cu), the default of a sharded
+ * context: per iteration an m-way ncclReduceScatter of the partial products'
+ * row chunks (+ a 1-double all-reduce of the fidelity), the W^-1 mix of this
+ * rank's chunk only, and an m-way ncclAllGather of the new configuration rows
+ * -- all on the context stream, inside the solve's CUDA graph.  SPMD after
+ * jofc_set_shard(ctx, rank, world) and the problem: rank 0 makes an id with
+ * jofc_nccl_unique_id, the caller broadcasts its JOFC_NCCL_ID_BYTES bytes,
+ * every rank calls jofc_nccl_init.  The world must divide the padded object
+ * count (any power of two up to 128).  NCCL is the process's libnccl.so.2
+ * (dlopen; the system NCCL when none is loaded yet).  Replaces the same
+ * data-parallel site as the reference's OpenMP loop over (modality, object),
+ * proj/src/solver.cpp:27-49. */
+#define JOFC_NCCL_ID_BYTES 128
+int jofc_nccl_version(int* version);
+int jofc_nccl_unique_id(void* id_out);
+int jofc_nccl_init(jofc_ctx* ctx, const void* id, int rank, int world);
+int jofc_nccl_release(jofc_ctx* ctx);
+
 /* Peer-memory exchange (NVLink / NVSwitch), the alternative to the all-reduce
  * hook: the exchange of the products (the hook's all-reduce + epilogue) becomes
  * two kernels that read the world's partial products and write the mixed

@@ -83,6 +83,10 @@ _SIGS = {
     "jofc_profile_read": (C.c_int, [_vp, _dp, C.POINTER(C.c_uint64)]),
     "jofc_set_exchange_buffer": (C.c_int, [_vp, _vp, _sz]),
     "jofc_exchange_count": (_sz, [_vp, _sz]),
+    "jofc_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
+    "jofc_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "jofc_nccl_init": (C.c_int, [_vp, C.c_char_p, C.c_int, C.c_int]),
+    "jofc_nccl_release": (C.c_int, [_vp]),
     "jofc_peer_export": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
     "jofc_peer_attach": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
     "jofc_peer_attach_pointers": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),

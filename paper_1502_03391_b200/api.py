@@ -295,6 +295,29 @@ class Device:
         self._hook = _capi.ALLREDUCE_FN(tramp)
         check(self.lib.jofc_set_allreduce(self.h, self._hook, None))
 
+    # C-native NCCL exchange (include/jofc_gpu.h, jofc_nccl_*): the default
+    # multi-GPU path; paper_1502_03391_b200.dist.attach_nccl_native runs the
+    # SPMD id broadcast / init sequence
+    @staticmethod
+    def nccl_unique_id():
+        buf = C.create_string_buffer(128)
+        check(_capi.load().jofc_nccl_unique_id(buf))
+        return buf.raw
+
+    @staticmethod
+    def nccl_version():
+        v = C.c_int()
+        check(_capi.load().jofc_nccl_version(C.byref(v)))
+        return int(v.value)
+
+    def nccl_init(self, uid, rank, world):
+        if len(uid) != 128:
+            raise InvalidArgument("NCCL exchange: the unique id is 128 bytes")
+        check(self.lib.jofc_nccl_init(self.h, uid, int(rank), int(world)))
+
+    def nccl_release(self):
+        check(self.lib.jofc_nccl_release(self.h))
+
     # peer-memory exchange (include/jofc_gpu.h, jofc_peer_*): multi-GPU
     # without the all-reduce hook; paper_1502_03391_b200.dist.attach_peers
     # runs the SPMD export / all-gather / attach sequence

@@ -229,6 +229,10 @@ struct jofc_ctx {
   cudaEvent_t stop_ev[2] = {nullptr, nullptr};
   // peer-memory exchange (multi-GPU without NCCL)
   jofc_gpu::capi::PeerState peer;
+  // C-native NCCL exchange (capi_nccl.cu): reduce-scatter of P, own-row mix,
+  // all-gather of X; ncclComm_t, kept opaque here
+  void* nccl_comm = nullptr;
+  int nccl_world = 0;
 };
 
 namespace jofc_gpu {
@@ -256,6 +260,12 @@ int prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
 int peer_stage(jofc_ctx* c, const PassParams& pp, size_t t, int stage);
 int peer_check(jofc_ctx* c);
 void peer_release(jofc_ctx* c);
+// NCCL exchange: the world divides n_pad; collectives of iteration t
+int nccl_check(jofc_ctx* c);
+long long nccl_chunk_rows(const jofc_ctx* c);
+int nccl_reduce(jofc_ctx* c, double* P, size_t fid_slot);
+int nccl_gather(jofc_ctx* c, double* xn);
+void nccl_release(jofc_ctx* c);
 
 }  // namespace capi
 }  // namespace jofc_gpu

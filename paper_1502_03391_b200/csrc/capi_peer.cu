@@ -221,6 +221,7 @@ int jofc_peer_attach(jofc_ctx* c, int rank, int world, const void* handles) {
     ps.opened.push_back(p);
     bases[q] = static_cast<double*>(p);
   }
+  nccl_release(c);  // one exchange at a time
   return attach_common(c, rank, world, bases);
 }
 
@@ -232,6 +233,7 @@ int jofc_peer_attach_pointers(jofc_ctx* c, int rank, int world, void* const* sla
   for (int q = 0; q < world; ++q) bases[q] = static_cast<double*>(slabs[q]);
   if (bases[rank] != c->peer.slab)
     return set_error(JOFC_EINVAL, "peer exchange: slab %d is not this context's", rank);
+  nccl_release(c);  // one exchange at a time
   return attach_common(c, rank, world, bases);
 }
 

@@ -113,6 +113,23 @@ Configuration unflatten(const std::vector<double>& x, std::size_t m, std::size_t
 
 void set_device(int device) { t_device = device; }
 
+std::vector<unsigned char> nccl_unique_id() {
+  std::vector<unsigned char> id(JOFC_NCCL_ID_BYTES);
+  check(jofc_nccl_unique_id(id.data()));
+  return id;
+}
+
+void set_shard(int rank, int world, const std::vector<unsigned char>& nccl_id) {
+  if (world > 1 && nccl_id.empty())
+    throw std::invalid_argument("set_shard: a sharded context needs the group's NCCL id");
+  if (!nccl_id.empty() && nccl_id.size() != JOFC_NCCL_ID_BYTES)
+    throw std::invalid_argument("set_shard: the NCCL id is 128 bytes");
+  Ctx& c = ctx();
+  check(jofc_set_shard(c.h, rank, world));  // (drops the resident problem)
+  c.problem = 0;
+  if (!nccl_id.empty()) check(jofc_nccl_init(c.h, nccl_id.data(), rank, world));
+}
+
 Configuration averaged_procrustes_init(const OmnibusProblem& problem, std::size_t d, bool) {
   Ctx& c = with_problem(problem, false);
   std::vector<double> x(problem.modality_count() * problem.object_count() * d);

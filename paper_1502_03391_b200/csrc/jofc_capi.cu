@@ -439,11 +439,19 @@ int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t 
   ep.n = L.n;
   ep.n_pad = L.n_pad;
   ep.fid_slot = fid_slot(c);
+  ep.mix_lo = 0;
+  ep.mix_hi = L.n;
+  if (c->nccl_comm) {  // this rank mixes its own row chunk (capi_nccl.cu)
+    JOFC_TRY(nccl_check(c));
+    const long long rows = nccl_chunk_rows(c);
+    ep.mix_lo = std::min<long long>(L.n, rows * c->rank);
+    ep.mix_hi = std::min<long long>(L.n, rows * (c->rank + 1));
+  }
 
   // Small problems on one GPU: the pass kernel's last CTA runs the epilogue
   // too (one launch per iteration instead of two).  The threshold keeps the
   // one-CTA epilogue below the cost of a second launch.
-  pp.fuse_epilogue = (c->world == 1 && L.n <= fuse_epilogue_max_n()) ? 1 : 0;
+  pp.fuse_epilogue = (c->world == 1 && !c->nccl_comm && L.n <= fuse_epilogue_max_n()) ? 1 : 0;
   pp.epi = ep;
   *ppo = pp;
   *epo = ep;
@@ -464,7 +472,19 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   // Single GPU, no per-launch events: replay a captured CUDA graph of the
   // whole 2(max_it + 1)-kernel sequence (kernel parameters only hold buffer
   // pointers; everything iteration-dependent lives in the control block).
-  const bool graphable = c->use_graphs && c->world == 1 && !events && !c->profiling;
+  // (the NCCL exchange is captured with the kernels: its calls are on the
+  // context stream with fixed buffers per iteration parity)
+  const bool nccl_x = c->nccl_comm != nullptr;
+  const bool graphable = c->use_graphs && (c->world == 1 || nccl_x) && !c->peer.active &&
+                         !events && !c->profiling;
+  // iteration t's collectives: the reduce-scatter after its pass, the
+  // all-gather of X_{t+1} after its epilogue
+  auto exchange_pre = [&]() -> int {
+    return nccl_x ? nccl_reduce(c, exchange(c), fid_slot(c)) : JOFC_OK;
+  };
+  auto exchange_post = [&](size_t t) -> int {
+    return nccl_x ? nccl_gather(c, xbuf(c, static_cast<int>((t + 1) & 1))) : JOFC_OK;
+  };
   if (early_stop && !c->stop_flag) {
     JOFC_CUDA(cudaMallocHost(&c->stop_flag, 2 * sizeof(int)));
     for (int k = 0; k < 2; ++k)
@@ -484,7 +504,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
     }
     return JOFC_OK;
   };
-  if (graphable && use_persistent(c)) {
+  if (graphable && !nccl_x && use_persistent(c)) {
     // (a cooperative launch is refused when the SMs are shared, e.g. under
     // MPS: the per-iteration launches below then run the solve)
     if (persistent_for_d(c, pp) == JOFC_OK) {
@@ -498,7 +518,10 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
     // one graph of the whole sequence, or (early stop) of one chunk replayed
     // until the device says done: later iterations are no-ops on the device
     // anyway (the control block), this stops paying their launches
-    const size_t per_graph = early_stop ? std::min(stop_chunk(), max_it + 1) : max_it + 1;
+    size_t per_graph = early_stop ? std::min(stop_chunk(), max_it + 1) : max_it + 1;
+    // a chunk graph replayed for later iterations must keep their X-buffer
+    // parity (the all-gather targets are baked in): even length
+    if (nccl_x && early_stop && per_graph < max_it + 1 && (per_graph & 1)) ++per_graph;
     std::vector<uintptr_t> key = {c->d, per_graph, static_cast<uintptr_t>(c->pass_grid),
                                   static_cast<uintptr_t>(c->epi_grid),
                                   reinterpret_cast<uintptr_t>(pp.delta),
@@ -513,7 +536,10 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
                                   static_cast<uintptr_t>(L.n), static_cast<uintptr_t>(L.m),
                                   static_cast<uintptr_t>(L.begin), static_cast<uintptr_t>(L.end),
                                   static_cast<uintptr_t>(pp.diag),
-                                  static_cast<uintptr_t>(pp.fuse_epilogue)};
+                                  static_cast<uintptr_t>(pp.fuse_epilogue),
+                                  reinterpret_cast<uintptr_t>(c->nccl_comm),
+                                  static_cast<uintptr_t>(ep.mix_lo),
+                                  static_cast<uintptr_t>(ep.mix_hi)};
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       if (c->graphs.size() >= 8) {
@@ -526,7 +552,9 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
       int lrc = JOFC_OK;
       for (size_t t = 0; t < per_graph && !lrc; ++t) {
         lrc = pass_for_d(c, pp);
+        if (!lrc) lrc = exchange_pre();
         if (!lrc && !fused) lrc = epi_for_d(c, ep);
+        if (!lrc) lrc = exchange_post(t);
       }
       cudaGraph_t g = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
@@ -545,7 +573,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
     }
     for (size_t ch = 0; ch * per_graph <= max_it; ++ch) {
       JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
-      c->launches += (fused ? 1 : 2) * per_graph;
+      c->launches += (fused ? 1 : 2) * per_graph;  // (our kernels; NCCL's not counted)
       if (early_stop) {
         bool stop = false;
         JOFC_TRY(chunk_done(ch, &stop));
@@ -577,7 +605,9 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
     if (rc) return rc;
     if (pe1) JOFC_CUDA(cudaEventRecord(pe1, c->stream));
     ++c->launches;
-    if (c->world > 1) {
+    if (nccl_x) {
+      JOFC_TRY(exchange_pre());
+    } else if (c->world > 1) {
       if (!c->allreduce)
         return set_error(JOFC_ECOMM, "sharded context (world %d) without an all-reduce hook",
                          c->world);
@@ -589,6 +619,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
       if (rc) return rc;
       ++c->launches;
     }
+    JOFC_TRY(exchange_post(t));
   }
   if (events) JOFC_CUDA(cudaEventRecord((*events)[max_it + 1], c->stream));
   c->max_it_enqueued = max_it;
@@ -662,6 +693,7 @@ int jofc_ctx_destroy(jofc_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   peer_release(c);
+  nccl_release(c);
   for (DevBuf<double>* b : {&c->delta, &c->x0, &c->x1, &c->P, &c->fid_part, &c->com_part,
                             &c->trace, &c->consts, &c->oos_x, &c->oos_delta, &c->oos_y0,
                             &c->oos_y1, &c->oos_part, &c->oos_trace})
@@ -747,6 +779,7 @@ int jofc_set_shard(jofc_ctx* c, int rank, int world) {
   JOFC_CUDA(cudaSetDevice(c->device));
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
   peer_release(c);  // a new shard needs a new problem and a new peer group
+  nccl_release(c);  // ... and a new communicator
   c->rank = rank;
   c->world = world;
   c->has_problem = false;

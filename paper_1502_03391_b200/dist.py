@@ -1,8 +1,11 @@
 """Multi-GPU plumbing for the sharded Guttman loop (one process per GPU).
 
-Two exchanges: attach_nccl (the all-reduce hook below) and attach_peers (the
-products and configuration rows move through peer memory inside the loop's
-own kernels, csrc/jofc_peer.cuh).
+Three exchanges: attach_nccl_native (the default: the C ABI's own NCCL
+reduce-scatter of the products + all-gather of X per iteration, captured in
+the solve's CUDA graph, csrc/capi_nccl.cu), attach_nccl (a Python all-reduce
+hook over torch.distributed, below) and attach_peers (the products and
+configuration rows move through peer memory inside the loop's own kernels,
+csrc/jofc_peer.cuh).
 
 Each rank owns a balanced contiguous range of the packed Delta block stream
 (jofc_set_shard); every iteration the partial product P = B(X)X (m*n_pad*d
@@ -51,6 +54,21 @@ def attach_nccl(dev, d, group=None):
     return buf
 
 
+def attach_nccl_native(dev, group=None):
+    """The C-native NCCL exchange (csrc/capi_nccl.cu): rank 0 makes an NCCL
+    unique id, torch.distributed broadcasts it, every rank's context joins the
+    communicator.  From then on each Guttman iteration's reduce-scatter of the
+    products and all-gather of the new configuration rows are issued by the C
+    ABI itself, on the context stream, inside the solve's CUDA graph -- no
+    Python in the loop."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [dev.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    dev.nccl_init(obj[0], rank, world)
+    dist.barrier(group=group)
+
+
 def exchange_handles(handle, group=None):
     """All-gather of one bytes object per rank (rank order)."""
     import torch.distributed as dist
@@ -68,6 +86,7 @@ def attach_peers(dev, group=None):
     handle, _ = dev.peer_export()
     handles = exchange_handles(handle, group)
     dev.peer_attach(dist.get_rank(group), len(handles), handles)
+    dist.barrier(group=group)  # every slab zeroed before any rank's first flag
     return handles
 
 

@@ -3,7 +3,9 @@
 // proj/tests/test_oos.cpp): seeded random problems, checks against an oracle.
 // The oracle is the C restatement (oracle/jofc_oracle.c), itself pinned
 // bit-for-bit to the reference by tests/test_oracle.py.  Exit code = failures.
+#include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <fstream>
 #include <limits>
@@ -296,6 +298,39 @@ static void out_of_sample() {
         }
 }
 
+static void sharded_nccl() {
+  // set_shard with an NCCL id: a one-rank group on this one-GPU box (the
+  // exchange's real NCCL calls inside the solve's graph) ends on the
+  // unsharded iterate; set_shard(0, 1, {}) returns to the plain context
+  Rng rng(93);
+  const std::size_t m = 2, n = 700, d = 3;
+  std::vector<DenseMatrix> mods;
+  const DenseMatrix z = random_matrix(rng, n, 3);
+  for (std::size_t l = 0; l < m; ++l) {
+    DenseMatrix f = z;
+    for (std::size_t i = 0; i < f.size(); ++i) f.data()[i] += 0.1 * rng.normal();
+    mods.push_back(edm(f));
+  }
+  const OmnibusProblem problem(mods);
+  const Configuration x0 = random_config(rng, n, m, d);
+  SolveOptions o;
+  o.dim = d;
+  o.eps = 1e-300;
+  o.max_iterations = 30;
+  o.init = InitKind::provided;
+  o.init_config = x0;
+  const EmbeddingResult plain = fjofc_embed(problem, WeightSpec::uniform(0.5), o);
+  set_shard(0, 1, nccl_unique_id());
+  const EmbeddingResult sh = fjofc_embed(problem, WeightSpec::uniform(0.5), o);
+  CHECK(sh.iterations == plain.iterations);
+  CHECK(rel_fro(flat(sh.config), flat(plain.config)) < 1e-12);
+  CHECK(rel(sh.stress_trace.back(), plain.stress_trace.back()) < 1e-12);
+  CHECK(throws<std::invalid_argument>([] { set_shard(1, 2, {}); }));
+  set_shard(0, 1, {});
+  const EmbeddingResult again = fjofc_embed(problem, WeightSpec::uniform(0.5), o);
+  CHECK(rel_fro(flat(again.config), flat(plain.config)) < 1e-12);
+}
+
 static double max_abs_mat(const DenseMatrix& a, const DenseMatrix& b) {
   double m = 0.0;
   for (std::size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a.data()[i] - b.data()[i]));
@@ -420,13 +455,58 @@ static void io_csv() {
         "cannot open '/tmp/jofc_dropin_missing.csv'");
 }
 
-int main() {
+// `dropin_parity oos IN OUT`: jofc::oos_embed (the drop-in entry point) for
+// k points of one problem read from IN -- u64 m, n, d, k; X (m x n x d);
+// deltas (k x m x n); u64 seeds[k]; f64 w, eps; u64 max_it -- writing per
+// point y (m x d), iterations (f64) and the stress trace (max_it + 1, NaN
+// padded) to OUT.  tests/test_gpu_oos_c5.py compares it with the reference.
+static int oos_file(const char* in_path, const char* out_path) {
+  std::ifstream in(in_path, std::ios::binary);
+  std::uint64_t hdr[4];
+  in.read(reinterpret_cast<char*>(hdr), sizeof hdr);
+  const std::size_t m = hdr[0], n = hdr[1], d = hdr[2], k = hdr[3];
+  std::vector<double> xf(m * n * d), df(k * m * n);
+  std::vector<std::uint64_t> seeds(k);
+  double w = 0.0, eps = 0.0;
+  std::uint64_t max_it = 0;
+  in.read(reinterpret_cast<char*>(xf.data()), xf.size() * sizeof(double));
+  in.read(reinterpret_cast<char*>(df.data()), df.size() * sizeof(double));
+  in.read(reinterpret_cast<char*>(seeds.data()), k * sizeof(std::uint64_t));
+  in.read(reinterpret_cast<char*>(&w), sizeof w);
+  in.read(reinterpret_cast<char*>(&eps), sizeof eps);
+  in.read(reinterpret_cast<char*>(&max_it), sizeof max_it);
+  if (!in) return 2;
+  Configuration x;
+  for (std::size_t l = 0; l < m; ++l) {
+    DenseMatrix b(n, d);
+    std::copy(xf.begin() + l * n * d, xf.begin() + (l + 1) * n * d, b.data());
+    x.blocks.push_back(std::move(b));
+  }
+  std::ofstream out(out_path, std::ios::binary);
+  for (std::size_t q = 0; q < k; ++q) {
+    OosDissimilarity dl;
+    for (std::size_t l = 0; l < m; ++l)
+      dl.deltas.emplace_back(df.begin() + (q * m + l) * n, df.begin() + (q * m + l + 1) * n);
+    const OosResult r = oos_embed(x, dl, w, OosOptions{eps, static_cast<std::size_t>(max_it)},
+                                  seeds[q]);
+    std::vector<double> rec(m * d + 1 + max_it + 1, std::numeric_limits<double>::quiet_NaN());
+    std::copy(r.y.data(), r.y.data() + m * d, rec.begin());
+    rec[m * d] = static_cast<double>(r.iterations);
+    std::copy(r.stress_trace.begin(), r.stress_trace.end(), rec.begin() + m * d + 1);
+    out.write(reinterpret_cast<const char*>(rec.data()), rec.size() * sizeof(double));
+  }
+  return out ? 0 : 3;
+}
+
+int main(int argc, char** argv) {
+  if (argc == 4 && std::string(argv[1]) == "oos") return oos_file(argv[2], argv[3]);
   fast_step_grid();
   solve_trajectory();
   realizable_converges();
   default_init_runs();
   errors();
   out_of_sample();
+  sharded_nccl();
   linear_algebra();
   io_csv();
   std::printf("dropin_parity: %d checks, %d failures\n", g_checks, g_fail);

@@ -87,3 +87,13 @@ def test_oos_deltas_are_edm_entries():
     full = P.distance_matrix(wl.features[0][: 40 + 3])
     for q in range(3):
         assert np.array_equal(od[q, 0], full[40 + q, :40])
+
+
+def test_nccl_resolves_at_run_time():
+    # NCCL is dlopen'ed (no link-time dependency); its version is readable
+    # without a GPU
+    import paper_1502_03391_b200 as jg
+    out = subprocess.run(["ldd", _capi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "libnccl" not in out
+    v = jg.Device.nccl_version()
+    assert v >= 22700, v

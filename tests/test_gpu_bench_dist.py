@@ -25,7 +25,10 @@ def free_port():
 
 
 def test_bench_torchrun_two_ranks_share_one_gpu():
-    env = dict(os.environ, JOFC_DIST_BACKEND="gloo", JOFC_BENCH_SHARE_GPU="1")
+    # (the Python all-reduce hook: NCCL, the default exchange, cannot put two
+    # ranks on one GPU)
+    env = dict(os.environ, JOFC_DIST_BACKEND="gloo", JOFC_BENCH_SHARE_GPU="1",
+               JOFC_EXCHANGE="hook")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "5", "--steps", "2",

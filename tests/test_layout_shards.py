@@ -181,3 +181,67 @@ def test_peer_decomposition_gloo_matches_oracle(world):
         assert np.linalg.norm(xn - ref_step) / np.linalg.norm(ref_step) < 1e-12
         assert abs(sigma - ref_stress) / ref_stress < 1e-12
     assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+
+
+def _nccl_worker(rank, world, port, payload, out):
+    # the C-native NCCL exchange (csrc/capi_nccl.cu) restated over gloo: P in
+    # the device layout (m x n_pad x d), an in-place reduce-scatter of each
+    # modality's row chunks (gloo has no reduce_scatter: all-reduce + own
+    # chunk, the same values), a fidelity all-reduce, the W^-1 mix of the OWN
+    # chunk's objects only, commensurability of the replicated X_t over all
+    # objects (every rank, same order), an all-gather of X_{t+1} row chunks
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    delta, x, within, coef, cross = payload
+    m, n, d = x.shape
+    n_pad = layout.ROWS * layout.geometry(n)[1]
+    assert n_pad % world == 0
+    chunk = n_pad // world
+    P, fid = partial_products(delta, x, within, m, n, rank, world)
+    Pd = np.zeros((m, n_pad, d))
+    Pd[:, :n] = P
+    own = slice(rank * chunk, (rank + 1) * chunk)
+    for l in range(m):  # reduce-scatter of modality l's row chunks
+        t = torch.from_numpy(Pd[l].copy())
+        dist.all_reduce(t)
+        Pd[l, own] = t.numpy()[own]
+    f = torch.tensor([fid], dtype=torch.float64)
+    dist.all_reduce(f)
+    lo, hi = min(n, rank * chunk), min(n, (rank + 1) * chunk)
+    xn = np.zeros((m, n_pad, d))
+    xn[:, lo:hi] = np.einsum("jl,lic->jic", coef, Pd[:, lo:hi])
+    com = sum(cross[a, b] * np.sum((x[a] - x[b]) ** 2) for a in range(m) for b in range(a + 1, m))
+    for l in range(m):  # all-gather of X_{t+1} row chunks
+        parts = [torch.zeros(chunk, d, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(xn[l, own].copy()))
+        xn[l] = torch.cat(parts).numpy()
+    out[rank] = (xn[:, :n], float(f[0]) + com)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_nccl_native_decomposition_gloo_matches_oracle(world):
+    from oracle.oracle import Port, Spec
+    P = Port()
+    rng = np.random.default_rng(7)
+    m, n, d = 3, 300, 3
+    delta = np.stack([P.distance_matrix(rng.normal(size=(n, 3))) for _ in range(m)])
+    x = rng.normal(size=(m, n, d))
+    spec = Spec.uniform(0.6)
+    within, cross = P.weights_expand(spec, m)
+    coef = P.script_w_inverse(spec, m, n) * within[None, :]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = 31500 + os.getpid() % 1000 + world
+    mp.spawn(_nccl_worker, args=(world, port, (delta, x, within, coef, cross), out),
+             nprocs=world, join=True)
+    ref_step = P.guttman_step_fast(delta, spec, x)
+    ref_stress = P.raw_stress(delta, spec, x)
+    for r in range(world):
+        xn, sigma = out[r]
+        assert np.linalg.norm(xn - ref_step) / np.linalg.norm(ref_step) < 1e-12
+        assert abs(sigma - ref_stress) / ref_stress < 1e-12
+    for r in range(1, world):  # replicated X and stop state on every rank
+        assert np.array_equal(out[r][0], out[0][0]) and out[r][1] == out[0][1]
