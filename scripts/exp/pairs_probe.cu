@@ -26,7 +26,7 @@ template <int D, int A, int C, int THREADS, int RACC>
 __global__ void __launch_bounds__(THREADS, 1) pairs_kernel(double* out, int blocks) {
   extern __shared__ double sm[];
   double* sd = sm;                      // 128 x 64 "delta" (column-major)
-  double* sx = sd + 128 * 64;           // 192 x D x rows of X
+  double* sx = sd + 128 * 64;           // 192 x D x rows of X (block: 128 rows x <= 64 columns)
   double* sr = sx + 192 * (D | 1);      // racc slots [a][cc][thread]
   for (int e = threadIdx.x; e < 128 * 64; e += THREADS) sd[e] = 1.0 + 1e-3 * (e % 97);
   for (int e = threadIdx.x; e < 192 * (D | 1); e += THREADS) sx[e] = 1e-2 * ((e * 37) % 101);
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(THREADS, 1) pairs_kernel(double* out, int bloc
   // tile of this thread: rows r0 + RS*a, columns c0 + CS*b
   constexpr int kRowLanes = 128 / A;       // threads along rows
   const int t = threadIdx.x;
-  const int rt = t % kRowLanes, ct = t / kRowLanes;  // ct < 64 / C
+  const int rt = t % kRowLanes, ct = t / kRowLanes;  // ct * C < 64
   double racc[RACC == 0 ? A : 1][D];
   if (RACC == 0)
 #pragma unroll
@@ -158,20 +158,16 @@ extern "C" int pairs_probe(int device) {
     fflush(stdout);                                                                           \
   }
   RUN(5, 8, 4, 256, 0)
-  RUN(5, 8, 4, 256, 1)
-  RUN(5, 4, 4, 512, 0)
-  RUN(5, 4, 4, 512, 1)
-  RUN(5, 8, 2, 512, 1)
-  RUN(5, 16, 2, 256, 0)
-  RUN(5, 16, 4, 128, 0)
-  RUN(5, 4, 8, 256, 0)
+  RUN(5, 8, 2, 384, 0)
+  RUN(5, 8, 2, 256, 0)
+  RUN(5, 4, 4, 384, 0)
+  RUN(5, 4, 2, 512, 0)
+  RUN(5, 8, 1, 512, 0)
+  RUN(5, 4, 4, 256, 0)
   RUN(3, 8, 4, 256, 0)
-  RUN(3, 8, 4, 256, 1)
+  RUN(3, 8, 2, 384, 0)
   RUN(3, 4, 4, 512, 0)
   RUN(3, 8, 2, 512, 0)
-  RUN(3, 8, 2, 512, 1)
-  RUN(3, 16, 2, 256, 0)
-  RUN(3, 16, 2, 256, 1)
 #undef RUN
   cudaFree(buf);
   return 0;
