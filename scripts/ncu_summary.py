@@ -57,6 +57,35 @@ def summarize_rep(rep):
     return res
 
 
+def stall_breakdown(rep):
+    """Warp-state samples by reason and by SASS opcode (ncu source page)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[1]
+    idx = {h: i for i, h in enumerate(hdr)}
+    cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+    by_reason, by_op = collections.Counter(), collections.defaultdict(collections.Counter)
+    total = 0
+    instrs = 0
+    for r in rows[2:]:
+        if len(r) < len(hdr):
+            continue
+        src = r[idx["Source"]].strip().split()
+        op = (src[1] if src and src[0].startswith("@") else (src[0] if src else "")).split(".")[0]
+        total += int(r[idx["# Samples"]] or 0)
+        instrs += int(r[idx["Instructions Executed"]] or 0)
+        for h in cols:
+            v = int(r[idx[h]] or 0)
+            by_reason[h[6:]] += v
+            by_op[op][h[6:]] += v
+    ops = sorted(by_op, key=lambda o: -sum(by_op[o].values()))[:12]
+    return {"samples": total, "warp_instructions": instrs,
+            "by_reason": {k: round(v / total, 4) for k, v in by_reason.most_common()},
+            "by_opcode": {o: {"share": round(sum(by_op[o].values()) / total, 4),
+                              "top": dict(by_op[o].most_common(3))} for o in ops}}
+
+
 def summarize_launches(path):
     rows = list(csv.reader(open(path)))
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
@@ -83,8 +112,11 @@ def main():
     ap.add_argument("out")
     ap.add_argument("--launches", action="store_true")
     ap.add_argument("--note", default="")
+    ap.add_argument("--stalls", action="store_true", help="add the source-page stall breakdown")
     a = ap.parse_args()
     data = summarize_launches(a.src) if a.launches else summarize_rep(a.src)
+    if a.stalls and not a.launches:
+        data = {"kernels": data, "stalls": stall_breakdown(a.src)}
     with open(a.out, "w") as f:
         json.dump({"source": a.src, "note": a.note, "data": data}, f, indent=1)
     print(json.dumps(data, indent=1)[:3000])
