@@ -816,13 +816,25 @@ int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta
   const Layout& L = c->lay;
   JOFC_CUDA(c->delta.ensure(static_cast<size_t>(std::max<long long>(L.local(), 1)) * kBlockElems));
 
-  // Frobenius norms over the full dense matrix in the reference's order.
+  // Frobenius norms over the full dense matrix (OmnibusProblem::normalized,
+  // proj/src/problem.cpp:34-42): row sums on all host threads, then added in
+  // row order -- deterministic and identical on every rank of a sharded
+  // context; it differs from the reference's one serial n^2 sum only by
+  // rounding (the serial loop took ~0.5 s per C3 modality).
   std::vector<double> norms(m, 0.0);
   if (normalize)
     for (size_t l = 0; l < m; ++l) {
-      double s = 0.0;
       const double* dl = delta[l];
-      for (size_t i = 0; i < n * n; ++i) s += dl[i] * dl[i];
+      std::vector<double> rows(n);
+#pragma omp parallel for schedule(static)
+      for (long long i = 0; i < static_cast<long long>(n); ++i) {
+        double s = 0.0;
+        const double* row = dl + static_cast<size_t>(i) * n;
+        for (size_t j = 0; j < n; ++j) s += row[j] * row[j];
+        rows[static_cast<size_t>(i)] = s;
+      }
+      double s = 0.0;
+      for (double v : rows) s += v;
       norms[l] = std::sqrt(s);
     }
 
