@@ -214,6 +214,7 @@ struct jofc_ctx {
   bool use_graphs = true;
   // oos state
   DevBuf<double> oos_x, oos_delta, oos_y0, oos_y1, oos_part, oos_trace;
+  DevBuf<double> oos_delta_t;  // [j][point group][n][32] (v2 pass)
   DevBuf<OosPoint> oos_st;
   DevBuf<unsigned> oos_done;
   // streaming ingest staging

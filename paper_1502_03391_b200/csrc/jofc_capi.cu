@@ -696,7 +696,7 @@ int jofc_ctx_destroy(jofc_ctx* c) {
   nccl_release(c);
   for (DevBuf<double>* b : {&c->delta, &c->x0, &c->x1, &c->P, &c->fid_part, &c->com_part,
                             &c->trace, &c->consts, &c->oos_x, &c->oos_delta, &c->oos_y0,
-                            &c->oos_y1, &c->oos_part, &c->oos_trace})
+                            &c->oos_y1, &c->oos_part, &c->oos_trace, &c->oos_delta_t})
     b->release();
   c->ctrl.release();
   c->up_bad.release();
@@ -1042,20 +1042,48 @@ int jofc_guttman_step(jofc_ctx* c, const jofc_weights* spec, size_t d, const dou
 // ---------------------------------------------------------------- out-of-sample
 namespace {
 
+// Kernels of the out-of-sample loop: 3 = one fused step kernel per update
+// (jofc_oos_step_kernel, default); 1 = pass (warp per point, lanes over rows)
+// + update kernel, the round-2 pair; 2 = the lanes-over-points pass on the
+// transposed delta + update kernel.  JOFC_OOS_KERNEL=1/2 for comparisons.
+int oos_kernel_version() {
+  static const int v = [] {
+    const char* e = std::getenv("JOFC_OOS_KERNEL");
+    return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 3;
+  }();
+  return v;
+}
+
 template <int D>
 int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
-  // 4 slices of the in-sample range (measured best at C5 among 2..16)
+  const bool v2 = oos_kernel_version() == 2;
+  const bool fused = oos_kernel_version() == 3;
+  // v1: 4 slices of the in-sample range (measured best at C5 among 2..16)
   const dim3 pg((op.k + kOosWarps - 1) / kOosWarps, op.m,
                 static_cast<unsigned>(std::min<long long>(kOosSplits, std::max<long long>(1, op.n / 256))));
+  // v2: (point group, modality) x slices -- one wave of resident CTAs
+  constexpr int smem2 = oos2_smem_bytes<D>();
+  int per_sm = 1;
+  if (v2) {
+    JOFC_CUDA(ensure_smem_attr(jofc_oos_pass2_kernel<D>, smem2, c->device));
+    JOFC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jofc_oos_pass2_kernel<D>,
+                                                            kOos2Warps * 32, smem2));
+  }
+  const long long gm = static_cast<long long>(op.groups) * op.m;
+  const long long slices = std::max<long long>(
+      1, std::min<long long>(op.n / kOos2Rows, std::max<long long>(1, per_sm) * c->num_sms / gm));
+  const dim3 pg2(static_cast<unsigned>(gm), static_cast<unsigned>(slices));
   const unsigned ug = (op.k + 127) / 128;
   // The launches are replayed from a captured CUDA graph of `per_graph` steps
   // (all per-step state is in the device-side point records), chunk after
   // chunk until every point is done: the count of finished points is read one
   // chunk behind, so at most ~2 chunks of no-op launches follow the last point.
   // (fixed iteration counts cannot stop early: one graph of all steps)
+  // (fused: launches 0 .. steps + 1, the last one only finishes the points)
+  const size_t launches_needed = static_cast<size_t>(steps) + (fused ? 2 : 1);
   const size_t chunk =
-      (stop_chunk() && !op.fixed) ? stop_chunk() : static_cast<size_t>(steps) + 1;
-  const size_t per_graph = std::min(chunk, static_cast<size_t>(steps) + 1);
+      (stop_chunk() && !op.fixed) ? stop_chunk() : launches_needed;
+  const size_t per_graph = std::min(chunk, launches_needed);
   if (!c->stop_flag) {
     JOFC_CUDA(cudaMallocHost(&c->stop_flag, 2 * sizeof(int)));
     for (int k = 0; k < 2; ++k)
@@ -1072,7 +1100,9 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
                                 reinterpret_cast<uintptr_t>(op.part),
                                 reinterpret_cast<uintptr_t>(op.st),
                                 reinterpret_cast<uintptr_t>(op.traces),
-                                reinterpret_cast<uintptr_t>(op.done_count)};
+                                reinterpret_cast<uintptr_t>(op.done_count),
+                                reinterpret_cast<uintptr_t>(op.deltas_t),
+                                static_cast<uintptr_t>(oos_kernel_version())};
   uint64_t wbits, ebits;
   std::memcpy(&wbits, &op.w, 8);
   std::memcpy(&ebits, &op.eps, 8);
@@ -1089,8 +1119,20 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
     if (smem > 48 * 1024)
       JOFC_CUDA(cudaFuncSetAttribute(jofc_oos_pass_kernel<D>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (fused && smem > 48 * 1024)
+      JOFC_CUDA(cudaFuncSetAttribute(jofc_oos_step_kernel<D>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     for (size_t t = 0; t < per_graph; ++t) {
-      jofc_oos_pass_kernel<D><<<pg, kOosWarps * 32, smem, c->stream>>>(op);
+      if (fused) {
+        OosParams ot = op;
+        ot.local_t = static_cast<int>(t);
+        jofc_oos_step_kernel<D><<<pg, kOosWarps * 32, smem, c->stream>>>(ot);
+        continue;
+      }
+      if (v2)
+        jofc_oos_pass2_kernel<D><<<pg2, kOos2Warps * 32, smem2, c->stream>>>(op);
+      else
+        jofc_oos_pass_kernel<D><<<pg, kOosWarps * 32, smem, c->stream>>>(op);
       jofc_oos_update_kernel<D><<<ug, 128, 0, c->stream>>>(op);
     }
     cudaGraph_t g = nullptr;
@@ -1104,9 +1146,15 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
       return set_error(JOFC_ECUDA, "oos graph instantiate failed: %s", cudaGetErrorString(ie));
     it = c->graphs.emplace(key, exec).first;
   }
-  for (size_t ch = 0; ch * per_graph <= static_cast<size_t>(steps); ++ch) {
+  for (size_t ch = 0; ch * per_graph < launches_needed; ++ch) {
+    if (fused) {  // this chunk's first launch index
+      jofc_oos_set_base_kernel<<<1, 1, 0, c->stream>>>(c->oos_done.p + 1,
+                                                       static_cast<unsigned>(ch * per_graph));
+      JOFC_CUDA(cudaGetLastError());
+      ++c->launches;
+    }
     JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
-    c->launches += 2 * per_graph;
+    c->launches += (fused ? 1 : 2) * per_graph;
     const int kk = static_cast<int>(ch & 1);
     JOFC_CUDA(cudaMemcpyAsync(&c->stop_flag[kk], op.done_count, sizeof(unsigned),
                               cudaMemcpyDeviceToHost, c->stream));
@@ -1131,21 +1179,39 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
   JOFC_CUDA(cudaSetDevice(c->device));
   JOFC_CUDA(c->oos_x.ensure(m * n * d + 4));  // + slack: chunk copies round up to 16 bytes
   JOFC_CUDA(c->oos_delta.ensure(k * m * n));
+  const int groups = static_cast<int>((k + 31) / 32);
+  if (oos_kernel_version() == 2)
+    JOFC_CUDA(c->oos_delta_t.ensure(static_cast<size_t>(groups) * 32 * m * n));
   JOFC_CUDA(c->oos_y0.ensure(k * m * d));
   JOFC_CUDA(c->oos_y1.ensure(k * m * d));
-  JOFC_CUDA(c->oos_part.ensure(k * m * (d + 2) + k));
+  // partials: 3 x k x m x (d + 2) (the fused step kernel's triple buffer; the
+  // two-kernel path uses the first) + 2 x k previous stresses
+  const size_t kmd = k * m * (d + 2);
+  JOFC_CUDA(c->oos_part.ensure(3 * kmd + 2 * k));
   JOFC_CUDA(c->oos_trace.ensure(k * (max_it + 1)));
   JOFC_CUDA(c->oos_st.ensure(k));
-  JOFC_CUDA(c->oos_done.ensure(1));
-  JOFC_CUDA(cudaMemsetAsync(c->oos_done.p, 0, sizeof(unsigned), c->stream));
+  JOFC_CUDA(c->oos_done.ensure(3));  // done count, launch index, arrivals
+  JOFC_CUDA(cudaMemsetAsync(c->oos_done.p, 0, 3 * sizeof(unsigned), c->stream));
   JOFC_CUDA(cudaMemcpyAsync(c->oos_x.p, x, m * n * d * sizeof(double), cudaMemcpyDefault, c->stream));
   JOFC_CUDA(cudaMemcpyAsync(c->oos_delta.p, deltas, k * m * n * sizeof(double), cudaMemcpyDefault,
                             c->stream));
   JOFC_CUDA(cudaMemcpyAsync(c->oos_y0.p, y0, k * m * d * sizeof(double), cudaMemcpyDefault,
                             c->stream));
   JOFC_CUDA(cudaMemsetAsync(c->oos_st.p, 0, k * sizeof(OosPoint), c->stream));
-  JOFC_CUDA(cudaMemsetAsync(c->oos_part.p, 0, (k * m * (d + 2) + k) * sizeof(double), c->stream));
+  JOFC_CUDA(cudaMemsetAsync(c->oos_part.p, 0, (3 * kmd + 2 * k) * sizeof(double), c->stream));
+  if (oos_kernel_version() == 2) {  // delta rows -> [j][point group][row][32 points], once per solve
+    const dim3 tg(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>(m * groups));
+    jofc_oos_transpose_kernel<<<tg, 256, 0, c->stream>>>(c->oos_delta.p, c->oos_delta_t.p,
+                                                         static_cast<int>(k), static_cast<int>(m),
+                                                         static_cast<long long>(n), groups);
+    JOFC_CUDA(cudaGetLastError());
+    ++c->launches;
+  }
   OosParams op{};
+  op.deltas_t = oos_kernel_version() == 2 ? c->oos_delta_t.p : nullptr;
+  op.groups = groups;
+  op.base = c->oos_done.p + 1;
+  op.prev2 = c->oos_part.p + 3 * kmd;
   op.x = c->oos_x.p;
   op.deltas = c->oos_delta.p;
   op.y0 = c->oos_y0.p;

@@ -44,7 +44,20 @@ struct OosParams {
   int max_it;
   int fixed;
   unsigned* done_count;  // points finished (the host stops enqueuing at k)
+  // v2 pass (lanes = points): delta transposed to [j][g][n][32], g = point group
+  const double* deltas_t;
+  int groups;
+  // fused step kernel: launch index = *base + local_t (base: one device word
+  // set per replayed chunk of launches; local_t: the launch's place in the
+  // captured chunk), the previous stress per point by parity (2 x k)
+  const unsigned* base;
+  int local_t;
+  double* prev2;
 };
+
+// The first launch index of a replayed chunk of fused steps (the value rides
+// in the kernel parameter: no host staging buffer).
+static __global__ void jofc_oos_set_base_kernel(unsigned* base, unsigned v) { *base = v; }
 
 constexpr int kOosWarps = 8;
 constexpr int kOosChunk = 512;
@@ -232,6 +245,362 @@ __global__ void __launch_bounds__(128) jofc_oos_update_kernel(const OosParams p)
   for (int e = 0; e < m * (D + 2); ++e) pz[e] = 0.0;
   st.t = t + 1;
   p.st[pt] = st;
+}
+
+// ------------------------------------------------------------- pass, v2
+// Lanes = points.  The batch's delta rows are transposed once per solve to
+// [modality j][point group g][in-sample row k][32 points] (jofc_oos_transpose_
+// kernel), so a chunk of R rows x 32 points is one contiguous 1-D bulk copy;
+// the matching R rows of X^(j) ride along.  CTA = (point group, modality,
+// slice of the in-sample range); its 8 warps take the chunk's rows
+// round-robin, every lane computing its own point's entry for the row
+// (x_k a shared-memory broadcast, delta a conflict-free 32-wide read) and
+// keeping psi, the fidelity and xi in registers -- no per-entry reductions,
+// and the ring keeps ~70 KB of delta in flight per CTA (the v1 kernel, one
+// warp per point with lanes over rows, was L2-latency bound: long-scoreboard
+// 40% of its samples).  The 8 warps' sums meet in shared memory; one add per
+// (point, modality, value) and CTA goes to `part`.
+constexpr int kOos2Rows = 64;
+constexpr int kOos2Warps = 8;
+template <int D>
+__host__ __device__ constexpr int oos2_stages() { return D >= 8 ? 3 : 4; }
+template <int D>
+__host__ __device__ constexpr int oos2_x_doubles() { return kOos2Rows * D + 2; }
+template <int D>
+__host__ __device__ constexpr int oos2_smem_bytes() {
+  return 128 + oos2_stages<D>() * (kOos2Rows * 32 + oos2_x_doubles<D>()) * 8 +
+         kOos2Warps * (D + 2) * 32 * 8;
+}
+
+static __global__ void __launch_bounds__(256) jofc_oos_transpose_kernel(const double* __restrict__ d,
+                                                                        double* __restrict__ dt,
+                                                                        int k, int m, long long n,
+                                                                        int groups) {
+  // CTA: (modality j, group g, 32-row tile of n); d is k x m x n
+  __shared__ double tile[32][33];
+  const int j = blockIdx.y / groups, g = blockIdx.y % groups;
+  const long long k0 = static_cast<long long>(blockIdx.x) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int q = ty; q < 32; q += 8) {  // read point q's rows k0 .. k0 + 31
+    const int pt = g * 32 + q;
+    const long long kk = k0 + tx;
+    tile[q][tx] = (pt < k && kk < n) ? d[(static_cast<long long>(pt) * m + j) * n + kk] : 0.0;
+  }
+  __syncthreads();
+  double* out = dt + ((static_cast<long long>(j) * groups + g) * n) * 32;
+  for (int r = ty; r < 32; r += 8) {
+    const long long kk = k0 + r;
+    if (kk < n) out[kk * 32 + tx] = tile[tx][r];
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kOos2Warps * 32) jofc_oos_pass2_kernel(const OosParams p) {
+  constexpr int kSt = oos2_stages<D>();
+  constexpr int R = kOos2Rows;
+  constexpr int XD = oos2_x_doubles<D>();
+  extern __shared__ __align__(128) unsigned char oos2_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(oos2_smem);
+  unsigned* done = reinterpret_cast<unsigned*>(oos2_smem + 64);
+  double* sd = reinterpret_cast<double*>(oos2_smem + 128);
+  double* sx = sd + kSt * R * 32;
+  double* sred = sx + kSt * XD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x % p.groups, j = blockIdx.x / p.groups;
+  const int pt = g * 32 + lane;
+  bool active = pt < p.k;
+  int t = 0;
+  if (active) {
+    const OosPoint st = p.st[pt];
+    active = !st.done;
+    t = st.t;
+  }
+  if (!__any_sync(0xffffffffu, active)) return;  // (the same 32 points in every warp)
+  const long long k_lo = p.n * blockIdx.y / gridDim.y;
+  const long long k_hi = p.n * (blockIdx.y + 1) / gridDim.y;
+  const int nch = static_cast<int>((k_hi - k_lo + R - 1) / R);
+  double y[D];
+  const double* yb = ((t & 1) ? p.y1 : p.y0) + (static_cast<long long>(pt) * p.m + j) * D;
+#pragma unroll
+  for (int c = 0; c < D; ++c) y[c] = active ? yb[c] : 0.0;
+  const double* dt = p.deltas_t + ((static_cast<long long>(j) * p.groups + g) * p.n) * 32;
+  const long long xbase = static_cast<long long>(j) * p.n * D;
+  auto issue = [&](int ch) {
+    const int st = ch % kSt;
+    const long long k0 = k_lo + static_cast<long long>(ch) * R;
+    const int rows = static_cast<int>(min(static_cast<long long>(R), k_hi - k0));
+    const uint32_t bd = static_cast<uint32_t>(rows) * 32u * 8u;
+    const long long first = xbase + k0 * D;
+    const long long start = first & ~1LL;  // 16-byte aligned
+    const uint32_t bx = static_cast<uint32_t>(((first - start + rows * D) * 8 + 15) & ~15LL);
+    mbar_expect_tx(&full[st], bd + bx);
+    bulk_g2s(sd + st * R * 32, dt + k0 * 32, bd, &full[st]);
+    bulk_g2s(sx + st * XD, p.x + start, bx, &full[st]);
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kSt; ++st) {
+      mbar_init(&full[st], 1);
+      done[st] = 0;
+    }
+    mbar_fence_init();
+    for (int ch = 0; ch < nch && ch < kSt; ++ch) issue(ch);
+  }
+  __syncthreads();
+  double psi = 0.0, fid = 0.0, xi[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) xi[c] = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int st = ch % kSt;
+    const long long k0 = k_lo + static_cast<long long>(ch) * R;
+    const int rows = static_cast<int>(min(static_cast<long long>(R), k_hi - k0));
+    mbar_wait(&full[st], static_cast<uint32_t>((ch / kSt) & 1));
+    const double* xs = sx + st * XD + ((xbase + k0 * D) & 1);
+    const double* ds = sd + st * R * 32 + lane;
+#pragma unroll 4
+    for (int rr = warp; rr < rows; rr += kOos2Warps) {
+      const double dv = ds[rr * 32];
+      double s = 0.0, xk[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        xk[c] = xs[rr * D + c];
+        const double df = xk[c] - y[c];
+        s = (c == 0) ? df * df : fma(df, df, s);
+      }
+      const double inv = (s > 0.0) ? rsqrt_nr(s) : 0.0;  // dist == 0 guard (proj/src/oos.cpp:88)
+      const double r = dv * inv;
+      const double resid = dv - s * inv;
+      fid = fma(resid, resid, fid);
+      psi += r;
+      const double cf = 1.0 - r;
+#pragma unroll
+      for (int c = 0; c < D; ++c) xi[c] = fma(cf, xk[c], xi[c]);
+    }
+    // the last warp done with the stage refills it (formal release/acquire as
+    // the in-sample ring)
+    __syncwarp();
+    if (lane == 0 && smem_arrive_count(&done[st]) == kOos2Warps - 1) {
+      done[st] = 0;
+      fence_acquire_cta();
+      if (ch + kSt < nch) {
+        fence_proxy_async_smem();
+        issue(ch + kSt);
+      }
+    }
+  }
+  // the 8 warps' partial sums of each point, then one add per value to `part`
+  double* mine = sred + warp * (D + 2) * 32 + lane;
+  mine[0] = psi;
+  mine[32] = fid;
+#pragma unroll
+  for (int c = 0; c < D; ++c) mine[(2 + c) * 32] = xi[c];
+  __syncthreads();
+  if (active) {
+    for (int v = warp; v < D + 2; v += kOos2Warps) {
+      double acc = 0.0;
+#pragma unroll
+      for (int w = 0; w < kOos2Warps; ++w) acc += sred[(w * (D + 2) + v) * 32 + lane];
+      red_add(p.part + (static_cast<long long>(pt) * p.m + j) * (D + 2) + v, acc);
+    }
+  }
+}
+
+// ------------------------------------------------------------- fused step
+// One kernel per Guttman update instead of pass + update: launch t first
+// applies update step s = t - 1 of every point its CTA touches -- sigma_s from
+// the triple-buffered partials part[s % 3] (proj/src/oos.cpp:50-70), the stop
+// rule (:221-226) and y_t (:98-111), each CTA redundantly for its own points
+// (a few dozen FP64 operations) -- then streams the pass for y_t into
+// part[t % 3].  The CTA of modality 0 and slice 0 of a point is its
+// bookkeeper: trace, previous stress (by parity), state, y_t to memory (the
+// next launch's start), part[(t + 1) % 3] zeroed (last read by launch t - 1).
+// The launch index is *base + local_t (a captured chunk of launches is
+// replayed with a new base).  The X chunks of the pass are requested before
+// the update step, so its loads overlap the first TMA copies.  Launch 0 is a
+// pure pass; launch max_it + 1 only finishes the points.  Decisions are
+// identical in every CTA: same inputs, same order.
+template <int D>
+__global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_step_kernel(const OosParams p) {
+  extern __shared__ __align__(128) unsigned char oos_smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(oos_smem);
+  double* xbuf = reinterpret_cast<double*>(oos_smem + 128);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pt = blockIdx.x * kOosWarps + warp;
+  const int j = blockIdx.y;
+  const int t = static_cast<int>(*p.base) + p.local_t;
+  const long long kmd = static_cast<long long>(p.k) * p.m * (D + 2);
+  const long long k_lo = p.n * blockIdx.z / gridDim.z;
+  const long long k_hi = p.n * (blockIdx.z + 1) / gridDim.z;
+  const int nch = static_cast<int>((k_hi - k_lo + kOosChunk - 1) / kOosChunk);
+  const long long xbase = static_cast<long long>(j) * p.n * D;
+  auto issue = [&](int ch) {
+    const long long k0 = k_lo + static_cast<long long>(ch) * kOosChunk;
+    const int rows = static_cast<int>(min(static_cast<long long>(kOosChunk), k_hi - k0));
+    const long long first = xbase + k0 * D;
+    const long long start = first & ~1LL;
+    const uint32_t bytes = static_cast<uint32_t>(((first - start + rows * D) * 8 + 15) & ~15LL);
+    mbar_expect_tx(&bar[ch & 1], bytes);
+    bulk_g2s(xbuf + (ch & 1) * oos_buf_doubles<D>(), p.x + start, bytes, &bar[ch & 1]);
+  };
+  // every CTA runs the chunk ring (a CTA whose points are all done only
+  // drains it): the X copies start before the update step's loads
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+    if (nch > 0) issue(0);
+    if (nch > 1) issue(1);
+  }
+  bool active = pt < p.k && !p.st[pt].done;
+  double y[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) y[c] = 0.0;
+  if (active && t == 0) {
+    const double* yb = p.y0 + (static_cast<long long>(pt) * p.m + j) * D;
+#pragma unroll
+    for (int c = 0; c < D; ++c) y[c] = yb[c];
+  } else if (active) {
+    // ---- update step s = t - 1 (every lane, same values)
+    const int s = t - 1;
+    const int m = p.m;
+    const double* part = p.part + (s % 3) * kmd + static_cast<long long>(pt) * m * (D + 2);
+    const double* yp = ((s & 1) ? p.y1 : p.y0) + static_cast<long long>(pt) * m * D;
+    double fid = 0.0, com = 0.0, xi_sum[D], psi_y[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xi_sum[c] = psi_y[c] = 0.0;
+    for (int l = 0; l < m; ++l) {
+      fid += part[l * (D + 2) + 1];
+      const double psi = part[l * (D + 2)];
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        xi_sum[c] += part[l * (D + 2) + 2 + c];
+        psi_y[c] = fma(psi, yp[l * D + c], psi_y[c]);
+      }
+      for (int l2 = l + 1; l2 < m; ++l2) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const double df = yp[l * D + c] - yp[l2 * D + c];
+          com = fma(df, df, com);
+        }
+      }
+    }
+    const double sigma = fid + p.w * com;
+    bool finished = false;
+    int status = 0;
+    if (!isfinite(sigma)) {
+      finished = true;
+      status = 2;
+    } else {
+      if (s >= 1 && !p.fixed && (p.prev2[((s - 1) & 1) * p.k + pt] - sigma) / p.term_count < p.eps)
+        finished = true;
+      if (s >= p.max_it) finished = true;
+    }
+    const bool keeper = j == 0 && blockIdx.z == 0 && lane == 0;
+    const double nn = static_cast<double>(p.n);
+    const double mw = static_cast<double>(m) * p.w;
+    const double direct = 1.0 / (nn + mw);
+    const double spread = p.w / (nn * (nn + mw));
+    if (!finished) {
+      const double psi_j = part[j * (D + 2)];
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+        y[c] = direct * (part[j * (D + 2) + 2 + c] + psi_j * yp[j * D + c]) +
+               spread * (xi_sum[c] + psi_y[c]);
+    }
+    if (keeper) {
+      if (p.traces) p.traces[static_cast<long long>(pt) * (p.max_it + 1) + s] = sigma;
+      p.prev2[(s & 1) * p.k + pt] = sigma;
+      double* yn = ((t & 1) ? p.y1 : p.y0) + static_cast<long long>(pt) * m * D;
+      if (!finished)
+        for (int l = 0; l < m; ++l) {
+          const double psi = part[l * (D + 2)];
+#pragma unroll
+          for (int c = 0; c < D; ++c)
+            yn[l * D + c] = direct * (part[l * (D + 2) + 2 + c] + psi * yp[l * D + c]) +
+                            spread * (xi_sum[c] + psi_y[c]);
+        }
+      double* pz = p.part + ((t + 1) % 3) * kmd + static_cast<long long>(pt) * m * (D + 2);
+      for (int e = 0; e < m * (D + 2); ++e) pz[e] = 0.0;
+      OosPoint st = p.st[pt];
+      st.t = t;
+      st.iterations = s;
+      if (finished) {
+        st.done = 1;
+        st.status = status;
+        atomicAdd(p.done_count, 1u);
+      }
+      p.st[pt] = st;
+    }
+    active = !finished;
+  }
+  // ---- pass for y_t (the v1 layout: warp = point, lanes over rows)
+  const double* dl = p.deltas + (static_cast<long long>(min(pt, p.k - 1)) * p.m + j) * p.n;
+  __syncthreads();
+  {
+    double psi[2] = {0.0, 0.0}, fid[2] = {0.0, 0.0}, xi[2][D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xi[0][c] = xi[1][c] = 0.0;
+    for (int ch = 0; ch < nch; ++ch) {
+      const long long k0 = k_lo + static_cast<long long>(ch) * kOosChunk;
+      const int rows = static_cast<int>(min(static_cast<long long>(kOosChunk), k_hi - k0));
+      mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
+      const double* xs = xbuf + (ch & 1) * oos_buf_doubles<D>() + ((xbase + k0 * D) & 1);
+      if (active) {
+        for (int kk0 = lane; kk0 < rows; kk0 += 32 * kOosUnroll) {
+          double dv[kOosUnroll];
+#pragma unroll
+          for (int u = 0; u < kOosUnroll; ++u) {
+            const int kk = kk0 + 32 * u;
+            dv[u] = (kk < rows) ? dl[k0 + kk] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kOosUnroll; ++u) {
+            const int kk = kk0 + 32 * u;
+            if (kk >= rows) break;
+            double sq = 0.0, xk[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              xk[c] = xs[kk * D + c];
+              const double df = xk[c] - y[c];
+              sq = (c == 0) ? df * df : fma(df, df, sq);
+            }
+            const double inv = (sq > 0.0) ? rsqrt_nr(sq) : 0.0;  // dist == 0 guard
+            const double r = dv[u] * inv;
+            const double resid = dv[u] - sq * inv;
+            const int a = u & 1;
+            fid[a] = fma(resid, resid, fid[a]);
+            psi[a] += r;
+            const double cf = 1.0 - r;
+#pragma unroll
+            for (int c = 0; c < D; ++c) xi[a][c] = fma(cf, xk[c], xi[a][c]);
+          }
+        }
+      }
+      __syncthreads();  // every warp is done with this buffer
+      if (threadIdx.x == 0 && ch + 2 < nch) {
+        fence_proxy_async_smem();
+        issue(ch + 2);
+      }
+    }
+    if (active) {
+      double spsi = psi[0] + psi[1], sfid = fid[0] + fid[1], sxi[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) sxi[c] = xi[0][c] + xi[1][c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        spsi += __shfl_xor_sync(0xffffffffu, spsi, o);
+        sfid += __shfl_xor_sync(0xffffffffu, sfid, o);
+#pragma unroll
+        for (int c = 0; c < D; ++c) sxi[c] += __shfl_xor_sync(0xffffffffu, sxi[c], o);
+      }
+      if (lane == 0) {
+        double* out = p.part + (t % 3) * kmd + (static_cast<long long>(pt) * p.m + j) * (D + 2);
+        red_add(out, spsi);
+        red_add(out + 1, sfid);
+#pragma unroll
+        for (int c = 0; c < D; ++c) red_add(out + 2 + c, sxi[c]);
+      }
+    }
+  }
 }
 
 }  // namespace jofc_gpu
