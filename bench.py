@@ -183,7 +183,8 @@ def run_ours(args):
     rank, world, local = env_rank()
     local = rank_device(local, torch)
     torch.cuda.set_device(local)
-    backend = init_dist(local, torch, dist) if world > 1 else None
+    backend = (init_dist(local, torch, dist)
+               if world > 1 or os.environ.get("JOFC_BENCH_NCCL_ONE_RANK") == "1" else None)
     cfg = args.config
     wl = workloads.make(cfg)
     spec = wl.spec
@@ -205,8 +206,10 @@ def run_ours(args):
     elif world > 1 and args.exchange == "hook":
         from paper_1502_03391_b200.dist import attach_nccl
         attach_nccl(dev, wl.d)  # torch-owned exchange buffer, NCCL all-reduce on dev.stream
-    elif world > 1:
+    elif world > 1 or (backend and os.environ.get("JOFC_BENCH_NCCL_ONE_RANK") == "1"):
         # the C ABI's own NCCL reduce-scatter + all-gather, in the CUDA graph
+        # (JOFC_BENCH_NCCL_ONE_RANK: a one-rank group under torchrun, the test
+        # hook a one-GPU box can run)
         from paper_1502_03391_b200.dist import attach_nccl_native
         attach_nccl_native(dev)
 
@@ -342,7 +345,7 @@ def run_ours(args):
                        "launch": "CUDA graph replay" if args.graphs else "stream launches",
                        "delta_bytes_resident_per_gpu": local_bytes,
                        "parallelism": f"delta-shard{world}" if world > 1 else "single",
-                       "collective": (None if world == 1 else
+                       "collective": (None if world == 1 and not backend else
                                       "peer memory: reduce-scatter read + mix + all-gather "
                                       "write in the loop's kernels (NVLink loads/stores)"
                                       if args.exchange == "peer" else
@@ -365,7 +368,7 @@ def run_ours(args):
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     dev.close()
-    if world > 1:
+    if backend:
         dist.destroy_process_group()
 
 

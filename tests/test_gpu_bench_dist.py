@@ -62,3 +62,22 @@ def test_bench_oos_points_split_over_two_ranks():
     out = json.loads(lines[0])
     assert out["n_gpus"] == 2 and out["value"] > 0
     assert "2 ranks" in out["config"]["parallelism"]
+
+
+def test_bench_torchrun_native_nccl_one_rank():
+    # the default multi-GPU exchange (the C ABI's NCCL reduce-scatter /
+    # all-gather, captured in the solve) through the torchrun path: a one-rank
+    # group, the only NCCL group a one-GPU box can form (NCCL refuses two
+    # ranks on one device)
+    env = dict(os.environ, JOFC_BENCH_NCCL_ONE_RANK="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "1", "--config", "5", "--steps", "2",
+           "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    out = json.loads(lines[-1])
+    assert "C-ABI NCCL" in out["config"]["collective"]
+    assert out["config"]["iterations_per_step"] == 100 and out["value"] > 0
+    assert out["e2e"]["x_final_rel_diff_vs_device_run"] < 1e-12
