@@ -1054,13 +1054,23 @@ int oos_kernel_version() {
   return v;
 }
 
+// Slices of the in-sample range per (point group, modality): kOosSplits, or
+// JOFC_OOS_SPLITS (experiments).
+long long oos_splits() {
+  static const long long v = [] {
+    const char* e = std::getenv("JOFC_OOS_SPLITS");
+    return e ? std::max(1LL, std::atoll(e)) : static_cast<long long>(kOosSplits);
+  }();
+  return v;
+}
+
 template <int D>
 int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
   const bool v2 = oos_kernel_version() == 2;
   const bool fused = oos_kernel_version() == 3;
   // v1: 4 slices of the in-sample range (measured best at C5 among 2..16)
   const dim3 pg((op.k + kOosWarps - 1) / kOosWarps, op.m,
-                static_cast<unsigned>(std::min<long long>(kOosSplits, std::max<long long>(1, op.n / 256))));
+                static_cast<unsigned>(std::min<long long>(oos_splits(), std::max<long long>(1, op.n / 256))));
   // v2: (point group, modality) x slices -- one wave of resident CTAs
   constexpr int smem2 = oos2_smem_bytes<D>();
   int per_sm = 1;
@@ -1070,8 +1080,13 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
                                                             kOos2Warps * 32, smem2));
   }
   const long long gm = static_cast<long long>(op.groups) * op.m;
+  static const long long waves = [] {  // CTAs of the v2 pass per resident slot (experiments)
+    const char* e = std::getenv("JOFC_OOS2_WAVES");
+    return e ? std::max(1LL, std::atoll(e)) : 1LL;
+  }();
   const long long slices = std::max<long long>(
-      1, std::min<long long>(op.n / kOos2Rows, std::max<long long>(1, per_sm) * c->num_sms / gm));
+      1, std::min<long long>(op.n / kOos2Rows,
+                             waves * std::max<long long>(1, per_sm) * c->num_sms / gm));
   const dim3 pg2(static_cast<unsigned>(gm), static_cast<unsigned>(slices));
   const unsigned ug = (op.k + 127) / 128;
   // The launches are replayed from a captured CUDA graph of `per_graph` steps

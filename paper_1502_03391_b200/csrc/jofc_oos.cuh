@@ -260,10 +260,16 @@ __global__ void __launch_bounds__(128) jofc_oos_update_kernel(const OosParams p)
 // warp per point with lanes over rows, was L2-latency bound: long-scoreboard
 // 40% of its samples).  The 8 warps' sums meet in shared memory; one add per
 // (point, modality, value) and CTA goes to `part`.
-constexpr int kOos2Rows = 64;
+#ifndef JOFC_OOS2_ROWS
+#define JOFC_OOS2_ROWS 64
+#endif
+#ifndef JOFC_OOS2_STAGES
+#define JOFC_OOS2_STAGES 4
+#endif
+constexpr int kOos2Rows = JOFC_OOS2_ROWS;
 constexpr int kOos2Warps = 8;
 template <int D>
-__host__ __device__ constexpr int oos2_stages() { return D >= 8 ? 3 : 4; }
+__host__ __device__ constexpr int oos2_stages() { return D >= 8 ? 3 : JOFC_OOS2_STAGES; }
 template <int D>
 __host__ __device__ constexpr int oos2_x_doubles() { return kOos2Rows * D + 2; }
 template <int D>
