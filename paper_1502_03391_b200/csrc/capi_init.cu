@@ -346,6 +346,7 @@ int require_full_problem(jofc_ctx* c) {
 extern "C" {
 
 int jofc_cmds(jofc_ctx* c, int modality, size_t d, double* x_out) {
+  const NvtxScope nvtx_scope("jofc_cmds");
   int rc = require_full_problem(c);
   if (rc) return rc;
   if (modality >= c->lay.m) return set_error(JOFC_EINVAL, "cmds: modality out of range");
@@ -394,6 +395,7 @@ int jofc_symmetric_top_eigenpairs_subspace(jofc_ctx* c, size_t n, const double* 
 }
 
 int jofc_init_imputed_cmds(jofc_ctx* c, size_t d, size_t dense_cap, double* x_out) {
+  const NvtxScope nvtx_scope("jofc_init_imputed_cmds");
   int rc = require_full_problem(c);
   if (rc) return rc;
   const size_t m = static_cast<size_t>(c->lay.m), n = static_cast<size_t>(c->lay.n);
@@ -416,6 +418,7 @@ int jofc_init_imputed_cmds(jofc_ctx* c, size_t d, size_t dense_cap, double* x_ou
 }
 
 int jofc_init_averaged_procrustes(jofc_ctx* c, size_t d, double* x_out) {
+  const NvtxScope nvtx_scope("jofc_init_averaged_procrustes");
   int rc = require_full_problem(c);
   if (rc) return rc;
   JOFC_CUDA(cudaSetDevice(c->device));

@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "jofc_gpu.h"
 #include "jofc_kernels.cuh"
 #include "jofc_oos.cuh"
@@ -33,6 +35,16 @@ constexpr size_t kStopChunk = 32;
 constexpr long long kPersistentMaxBlocks = 4096;
 
 inline thread_local std::string g_error;
+
+// NVTX range over one C-ABI call (header-only NVTX v3: no link dependency;
+// free when no tool is attached).  The per-iteration device work is visible
+// to a profiler as kernels; these mark the API calls around them.
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
 
 inline int set_error(int code, const char* fmt, ...) {
   char buf[1024];
@@ -266,6 +278,7 @@ int nccl_check(jofc_ctx* c);
 long long nccl_chunk_rows(const jofc_ctx* c);
 int nccl_reduce(jofc_ctx* c, double* P, size_t fid_slot);
 int nccl_gather(jofc_ctx* c, double* xn);
+int nccl_wait(jofc_ctx* c);
 void nccl_release(jofc_ctx* c);
 
 }  // namespace capi

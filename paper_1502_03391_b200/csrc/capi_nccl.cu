@@ -30,8 +30,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstring>
 #include <mutex>
+#include <thread>
 
 #include "capi_internal.h"
 #include "jofc_gpu.h"
@@ -57,6 +59,7 @@ struct NcclApi {
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*GetVersion)(int*) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   std::string error;
 };
 
@@ -86,7 +89,8 @@ const NcclApi& nccl() {
               bind(h, "ncclAllReduce", api.AllReduce) &&
               bind(h, "ncclGroupStart", api.GroupStart) && bind(h, "ncclGroupEnd", api.GroupEnd) &&
               bind(h, "ncclGetErrorString", api.GetErrorString) &&
-              bind(h, "ncclGetVersion", api.GetVersion);
+              bind(h, "ncclGetVersion", api.GetVersion) &&
+              bind(h, "ncclCommGetAsyncError", api.CommGetAsyncError);
     if (!ok) {
       api.error = "libnccl.so.2 lacks a required symbol";
       return;
@@ -149,6 +153,39 @@ int nccl_gather(jofc_ctx* c, double* xn) {
                             static_cast<ncclComm_t>(c->nccl_comm), c->stream));
   }
   JOFC_NCCL(api.GroupEnd());
+  return JOFC_OK;
+}
+
+// Waits for the context stream of an NCCL-exchanging context.  A plain
+// cudaStreamSynchronize would block forever if a peer died or the network
+// failed (the collective kernels never complete), so the stream is polled and
+// the communicator's asynchronous error checked between polls; on an error
+// the communicator is aborted (which lets the stream drain) and released, and
+// the call returns JOFC_ECOMM -- the caller re-initialises the exchange.
+int nccl_wait(jofc_ctx* c) {
+  const NcclApi& api = nccl();
+  auto comm = static_cast<ncclComm_t>(c->nccl_comm);
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady)
+      return set_error(JOFC_ECUDA, "stream wait: %s", cudaGetErrorString(q));
+    ncclResult_t async = ncclSuccess;
+    const ncclResult_t r = api.CommGetAsyncError(comm, &async);
+    if (r != ncclSuccess || async != ncclSuccess) {
+      const ncclResult_t bad = (r != ncclSuccess) ? r : async;
+      api.CommAbort(comm);
+      c->nccl_comm = nullptr;
+      c->nccl_world = 0;
+      for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+      c->graphs.clear();
+      return set_error(JOFC_ECOMM, "NCCL exchange failed: %s (communicator aborted; call "
+                       "jofc_nccl_init again)", api.GetErrorString(bad));
+    }
+    // spin briefly (a solve ends within microseconds of the first poll when
+    // the host enqueued it long ago), then back off to 50 us sleeps
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
   return JOFC_OK;
 }
 

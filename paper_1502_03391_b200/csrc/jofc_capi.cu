@@ -632,7 +632,10 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
 int jofc_gpu::capi::finish_solve(jofc_ctx* c, Control* out) {
   JOFC_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl.p, sizeof(Control), cudaMemcpyDeviceToHost,
                             c->stream));
-  JOFC_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->nccl_comm)
+    JOFC_TRY(nccl_wait(c));  // polls the communicator's async error meanwhile
+  else
+    JOFC_CUDA(cudaStreamSynchronize(c->stream));
   *out = *c->ctrl_host;
   if (c->peer.active && c->peer.pending) {
     // the last evaluated iteration T left P region (T + phase) & 1 dirty and
@@ -804,6 +807,7 @@ double jofc_problem_pairs(jofc_ctx* c) {
 }
 
 int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta, int normalize) {
+  const NvtxScope nvtx_scope("jofc_set_problem");
   if (!c) return set_error(JOFC_EINVAL, "null context");
   if (m == 0) return set_error(JOFC_EINVAL, "OmnibusProblem: at least one modality required");
   if (n < 2) return set_error(JOFC_EINVAL, "OmnibusProblem: need at least two objects");
@@ -910,6 +914,7 @@ int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta
 }
 
 int jofc_set_problem_features(jofc_ctx* c, size_t m, size_t n, size_t p, const double* feats) {
+  const NvtxScope nvtx_scope("jofc_set_problem_features");
   if (!c) return set_error(JOFC_EINVAL, "null context");
   if (m == 0 || n < 2 || p == 0 || !feats)
     return set_error(JOFC_EINVAL, "features: need m >= 1, n >= 2, p >= 1");
@@ -942,6 +947,7 @@ int jofc_set_problem_features(jofc_ctx* c, size_t m, size_t n, size_t p, const d
 
 int jofc_fjofc_enqueue(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x0,
                        double eps, size_t max_it) {
+  const NvtxScope nvtx_scope("jofc_fjofc_enqueue");
   if (!c) return set_error(JOFC_EINVAL, "null context");
   JOFC_CUDA(cudaSetDevice(c->device));
   return enqueue_solve(c, spec, d, x0, eps, max_it, nullptr);
@@ -949,6 +955,7 @@ int jofc_fjofc_enqueue(jofc_ctx* c, const jofc_weights* spec, size_t d, const do
 
 int jofc_fetch_result(jofc_ctx* c, double* x_out, double* trace_out, size_t* iterations,
                       int* converged) {
+  const NvtxScope nvtx_scope("jofc_fetch_result");
   int rc = require_problem(c);
   if (rc) return rc;
   if (!c->ctrl.p) return set_error(JOFC_EINVAL, "fetch: no solve was enqueued");
@@ -971,6 +978,7 @@ int jofc_fetch_result(jofc_ctx* c, double* x_out, double* trace_out, size_t* ite
 int jofc_fjofc_embed(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x0, double eps,
                      size_t max_it, double* x_out, double* trace_out, size_t* iterations,
                      int* converged, double* step_seconds) {
+  const NvtxScope nvtx_scope("jofc_fjofc_embed");
   if (!c) return set_error(JOFC_EINVAL, "null context");
   JOFC_CUDA(cudaSetDevice(c->device));
   // step_seconds: two events around the whole solve (it keeps the CUDA-graph
@@ -1185,6 +1193,7 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
 int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x,
             const double* deltas, double w, const double* y0, double eps, size_t max_it,
             int fixed, double* y_out, double* traces, size_t* iterations, double* stress0) {
+  const NvtxScope nvtx_scope("jofc_oos");
   if (!c) return set_error(JOFC_EINVAL, "null context");
   if (!(w > 0.0)) return set_error(JOFC_EINVAL, "oos: w must be strictly positive");
   if (!(eps > 0.0)) return set_error(JOFC_EINVAL, "OosOptions: eps must be positive");
