@@ -140,6 +140,19 @@ int jofc_stress_evaluations(jofc_ctx* ctx, uint64_t* evaluations);
  * pass time (ms) and launch count since the last read. */
 int jofc_profile(jofc_ctx* ctx, int enable);
 int jofc_profile_read(jofc_ctx* ctx, double* pass_ms, uint64_t* pass_launches);
+/* How a solve evaluates the fidelity part of sigma(X_t).  AUTO (default):
+ * on the one-GPU route with a separate epilogue kernel (n > 1024 and more than
+ * 4096 packed blocks, or stream launches), iterations t >= 1 use the SMACOF
+ * identity F = sum delta^2 + sum d^2 - 2 tr(X'B(X)X) from the products the
+ * transform computes anyway (no per-pair fidelity work in the pass); once a
+ * modality's F falls below 1e-5 of A + S + 2|R| the rest of the solve sums
+ * (delta - d)^2 pair by pair (trace error < ~5e-11 relative either way).
+ * DIRECT: always pair by pair (every route other than the one above is).
+ * The environment JOFC_FIDELITY=direct forces DIRECT process-wide. */
+#define JOFC_FIDELITY_AUTO 0
+#define JOFC_FIDELITY_DIRECT 1
+int jofc_set_fidelity_form(jofc_ctx* ctx, int form);
+
 /* Multi-GPU: let the caller own the product/exchange buffer (device memory of
  * this context's GPU, >= m*n_pad*d + 1 doubles with n_pad = 64*ceil(n/64)) so
  * that its collective library can reduce it in place.  NULL reverts. */

@@ -284,6 +284,16 @@ class Device:
         check(self.lib.jofc_stress_evaluations(self.h, C.byref(v)))
         return int(v.value)
 
+    def set_fidelity_form(self, direct: bool):
+        """False (default): identity-form fidelity where the route allows it
+        (include/jofc_gpu.h, jofc_set_fidelity_form); True: always per pair."""
+        check(self.lib.jofc_set_fidelity_form(self.h, 1 if direct else 0))
+
+    def profile(self, enable: bool):
+        """CUDA events around every pass launch (also forces per-iteration
+        stream launches: no CUDA graph, no single-launch persistent solve)."""
+        check(self.lib.jofc_profile(self.h, 1 if enable else 0))
+
     def set_allreduce(self, fn):
         """fn(ptr: int, count: int, stream: int) -> None, sums in place over ranks."""
         def tramp(buf, count, stream, user):

@@ -327,6 +327,7 @@ int load_files(jofc_ctx* c, const std::vector<std::string>& paths, int normalize
       c->launches += 2;
     }
   }
+  JOFC_TRY(delta_sumsq(c));
   const auto t_s0 = clk::now();
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
   if (trace)

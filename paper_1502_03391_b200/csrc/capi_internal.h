@@ -204,6 +204,11 @@ struct jofc_ctx {
   bool has_problem = false;
   Layout lay;
   DevBuf<double> delta;
+  // A_l (sum of squared stored entries per modality, this shard) of the
+  // identity-form fidelity; computed by delta_sumsq() whenever Delta changes
+  DevBuf<double> sumsq, sumsq_part;
+  DevBuf<double> rho_part;  // epilogue partials of the identity form
+  int fidelity_form = JOFC_FIDELITY_AUTO;
   // solve state (sized for the current d)
   size_t d = 0;
   DevBuf<double> x0, x1, P, fid_part, com_part, trace, consts;
@@ -254,6 +259,11 @@ namespace capi {
 int copy_sync(jofc_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
 int prof_begin(jofc_ctx* c, cudaEvent_t* end);
 int require_problem(jofc_ctx* c);
+// A_l of the resident Delta into c->sumsq (enqueued on the context stream);
+// every path that (re)writes c->delta calls it before setting has_problem
+int delta_sumsq(jofc_ctx* c);
+// identity-form fidelity allowed (JOFC_FIDELITY=direct turns it off)
+bool rho_enabled();
 int diag_mode();
 size_t stop_chunk();
 long long fuse_epilogue_max_n();

@@ -68,6 +68,28 @@ int prof_begin(jofc_ctx* c, cudaEvent_t* end) {
   return JOFC_OK;
 }
 
+int delta_sumsq(jofc_ctx* c) {
+  const Layout& L = c->lay;
+  const int G = c->num_sms;
+  JOFC_CUDA(c->sumsq.ensure(L.m));
+  JOFC_CUDA(c->sumsq_part.ensure(static_cast<size_t>(G) * L.m));
+  jofc_modality_sumsq_kernel<<<dim3(G, L.m), 256, 0, c->stream>>>(c->delta.p, L.bpm, L.begin,
+                                                                   L.end, c->sumsq_part.p);
+  JOFC_CUDA(cudaGetLastError());
+  jofc_fold_partials_kernel<<<1, 128, 0, c->stream>>>(c->sumsq_part.p, G, L.m, c->sumsq.p);
+  JOFC_CUDA(cudaGetLastError());
+  c->launches += 2;
+  return JOFC_OK;
+}
+
+bool rho_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("JOFC_FIDELITY");
+    return !(e && std::string(e) == "direct");
+  }();
+  return v;
+}
+
 int require_problem(jofc_ctx* c) {
   if (!c) return set_error(JOFC_EINVAL, "null context");
   if (!c->has_problem) return set_error(JOFC_EINVAL, "no problem uploaded (jofc_set_problem)");
@@ -452,6 +474,19 @@ int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t 
   // too (one launch per iteration instead of two).  The threshold keeps the
   // one-CTA epilogue below the cost of a second launch.
   pp.fuse_epilogue = (c->world == 1 && !c->nccl_comm && L.n <= fuse_epilogue_max_n()) ? 1 : 0;
+  // Identity-form fidelity (jofc_kernels.cuh, rho_decide): the one-GPU route
+  // with a separate epilogue kernel.  (The fused and persistent epilogues,
+  // the NCCL, hook and peer exchanges keep the per-pair sum.)
+  if (rho_enabled() && c->fidelity_form == JOFC_FIDELITY_AUTO && c->world == 1 && !c->nccl_comm && !c->peer.active && !pp.fuse_epilogue &&
+      c->sumsq.p) {
+    const size_t K = 1 + static_cast<size_t>(L.m) * (d + 2);
+    JOFC_CUDA(c->rho_part.ensure((static_cast<size_t>(c->epi_grid) + 1) * K));
+    ep.rho = 1;
+    ep.rho_partials = c->rho_part.p;
+    ep.sumsq = c->sumsq.p;
+    ep.within = c->consts.p + 3 * mm;
+  }
+  pp.rho = ep.rho;
   pp.epi = ep;
   *ppo = pp;
   *epo = ep;
@@ -539,7 +574,10 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
                                   static_cast<uintptr_t>(pp.fuse_epilogue),
                                   reinterpret_cast<uintptr_t>(c->nccl_comm),
                                   static_cast<uintptr_t>(ep.mix_lo),
-                                  static_cast<uintptr_t>(ep.mix_hi)};
+                                  static_cast<uintptr_t>(ep.mix_hi),
+                                  static_cast<uintptr_t>(ep.rho),
+                                  reinterpret_cast<uintptr_t>(ep.rho_partials),
+                                  reinterpret_cast<uintptr_t>(ep.sumsq)};
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       if (c->graphs.size() >= 8) {
@@ -905,6 +943,7 @@ int jofc_set_problem(jofc_ctx* c, size_t m, size_t n, const double* const* delta
       ++chunk;
     }
   }
+  JOFC_TRY(delta_sumsq(c));
   int hbad = 0;
   JOFC_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
@@ -939,6 +978,7 @@ int jofc_set_problem_features(jofc_ctx* c, size_t m, size_t n, size_t p, const d
     JOFC_CUDA(cudaGetLastError());
     ++c->launches;
   }
+  JOFC_TRY(delta_sumsq(c));
   JOFC_CUDA(cudaStreamSynchronize(c->stream));
   f.release();
   c->has_problem = true;
@@ -1007,6 +1047,14 @@ int jofc_fjofc_embed(jofc_ctx* c, const jofc_weights* spec, size_t d, const doub
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
   return rc;
+}
+
+int jofc_set_fidelity_form(jofc_ctx* c, int form) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  if (form != JOFC_FIDELITY_AUTO && form != JOFC_FIDELITY_DIRECT)
+    return set_error(JOFC_EINVAL, "fidelity form %d unknown (0 auto, 1 direct)", form);
+  c->fidelity_form = form;
+  return JOFC_OK;
 }
 
 int jofc_raw_stress(jofc_ctx* c, const jofc_weights* spec, size_t d, const double* x,
