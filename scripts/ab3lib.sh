@@ -5,7 +5,7 @@ for rep in 1 2 3; do
   for lib in "$@"; do
     for c in $CFGS; do
       echo -n "$(basename $lib) "
-      JOFC_GPU_LIB=$lib timeout 300 python scripts/diag_pass.py --config $c --modes 0 2>&1 | tail -1
+      JOFC_GPU_LIB=$lib timeout 300 python scripts/diag_pass.py --config $c --modes 0 --its ${ITS:-0} 2>&1 | tail -1
     done
   done
 done

@@ -23,6 +23,9 @@ def main():
     ap.add_argument("--modes", default="0,1,2,3")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--its", type=int, default=0,
+                    help="iterations per solve (0: single-pass solves; >0 times every pass of "
+                         "real solves: iteration 0 per-pair fidelity, later ones identity form)")
     a = ap.parse_args()
     modes = [int(x) for x in a.modes.split(",")]
     if len(modes) > 1 or os.environ.get("JOFC_DIAG", str(modes[0])) != str(modes[0]):
@@ -30,7 +33,7 @@ def main():
         import subprocess
         for mode in modes:
             argv = [sys.executable, os.path.abspath(__file__), "--config", str(a.config),
-                    "--modes", str(mode), "--iters", str(a.iters)]
+                    "--modes", str(mode), "--iters", str(a.iters), "--its", str(a.its)]
             if a.n:
                 argv += ["--n", str(a.n)]
             subprocess.run(argv, env=dict(os.environ, JOFC_DIAG=str(mode)), check=True)
@@ -46,9 +49,9 @@ def main():
         # when the experiment corrupts the iterate
         for rep in range(2):
             check(lib.jofc_profile(dev.h, 1))
-            for _ in range(a.iters):
+            for _ in range(max(1, a.iters // (a.its + 1))):
                 check(lib.jofc_fjofc_enqueue(dev.h, C.byref(wl.spec.c()), wl.d, dptr(x0), 1e-300,
-                                             0))
+                                             a.its))
             ms, n = C.c_double(), C.c_uint64()
             check(lib.jofc_profile_read(dev.h, C.byref(ms), C.byref(n)))
         avg = ms.value / n.value
