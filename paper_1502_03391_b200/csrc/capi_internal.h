@@ -287,7 +287,7 @@ void peer_release(jofc_ctx* c);
 int nccl_check(jofc_ctx* c);
 long long nccl_chunk_rows(const jofc_ctx* c);
 int nccl_reduce(jofc_ctx* c, double* P, size_t fid_slot);
-int nccl_gather(jofc_ctx* c, double* xn);
+int nccl_gather(jofc_ctx* c, double* xn, double* sums = nullptr, size_t count = 0);
 int nccl_wait(jofc_ctx* c);
 void nccl_release(jofc_ctx* c);
 

@@ -17,6 +17,12 @@
 //                             same decision on every rank
 //   NCCL group: m x ncclAllGather(own rows of X_{t+1}_l -> X_{t+1}_l, in place)
 //
+// With the identity-form fidelity (jofc_kernels.cuh, rho_decide) the pass
+// skips the per-pair fidelity; the epilogue folds its own rows' sums
+// (commensurability, x_i . P_i, |x_i - x_0|^2, x_i - x_0 per modality), the
+// all-gather group all-reduces that vector (1 + m (d + 2) doubles), and
+// jofc_rho_decide_kernel takes the same decision on every rank.
+//
 // so each rank moves (W-1)/W of P in and of X out per iteration -- the
 // north star's all-gather of X -- and mixes 1/W of the objects.  Every call is
 // on the context stream, so the whole sequence is captured in the same CUDA
@@ -141,8 +147,10 @@ int nccl_reduce(jofc_ctx* c, double* P, size_t fid_slot) {
   return JOFC_OK;
 }
 
-// After the epilogue of t: all-gather of the own rows of X_{t+1}.
-int nccl_gather(jofc_ctx* c, double* xn) {
+// After the epilogue of t: all-gather of the own rows of X_{t+1}, plus (the
+// identity-form fidelity) the all-reduce of the ranks' folded sums, `sums`
+// (count doubles; null: none) in the same group.
+int nccl_gather(jofc_ctx* c, double* xn, double* sums, size_t count) {
   const NcclApi& api = nccl();
   const size_t cnt = static_cast<size_t>(nccl_chunk_rows(c)) * c->d;
   const size_t per_mod = static_cast<size_t>(c->lay.n_pad) * c->d;
@@ -152,6 +160,9 @@ int nccl_gather(jofc_ctx* c, double* xn) {
     JOFC_NCCL(api.AllGather(Xl + c->rank * cnt, Xl, cnt, ncclFloat64,
                             static_cast<ncclComm_t>(c->nccl_comm), c->stream));
   }
+  if (sums)
+    JOFC_NCCL(api.AllReduce(sums, sums, count, ncclFloat64, ncclSum,
+                            static_cast<ncclComm_t>(c->nccl_comm), c->stream));
   JOFC_NCCL(api.GroupEnd());
   return JOFC_OK;
 }

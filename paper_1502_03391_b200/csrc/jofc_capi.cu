@@ -229,6 +229,13 @@ int launch_epi(jofc_ctx* c, const EpiParams& ep) {
   return JOFC_OK;
 }
 
+template <int D>
+int launch_rho_decide(jofc_ctx* c, const EpiParams& ep) {
+  jofc_rho_decide_kernel<D><<<1, 32, 0, c->stream>>>(ep, static_cast<unsigned>(c->epi_grid));
+  JOFC_CUDA(cudaGetLastError());
+  return JOFC_OK;
+}
+
 
 
 
@@ -268,6 +275,9 @@ bool use_persistent(const jofc_ctx* c) {
 
 int setup_for_d(jofc_ctx* c) { JOFC_DISPATCH_D(c->d, setup_for, c); }
 int epi_for_d(jofc_ctx* c, const EpiParams& ep) { JOFC_DISPATCH_D(c->d, launch_epi, c, ep); }
+int rho_decide_for_d(jofc_ctx* c, const EpiParams& ep) {
+  JOFC_DISPATCH_D(c->d, launch_rho_decide, c, ep);
+}
 
 
 
@@ -477,11 +487,12 @@ int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t 
   // Identity-form fidelity (jofc_kernels.cuh, rho_decide): the one-GPU route
   // with a separate epilogue kernel.  (The fused and persistent epilogues,
   // the NCCL, hook and peer exchanges keep the per-pair sum.)
-  if (rho_enabled() && c->fidelity_form == JOFC_FIDELITY_AUTO && c->world == 1 && !c->nccl_comm && !c->peer.active && !pp.fuse_epilogue &&
-      c->sumsq.p) {
-    const size_t K = 1 + static_cast<size_t>(L.m) * (d + 2);
+  if (rho_enabled() && c->fidelity_form == JOFC_FIDELITY_AUTO &&
+      (c->world == 1 || c->nccl_comm) && !c->peer.active && !pp.fuse_epilogue && c->sumsq.p) {
+    const size_t K = 1 + static_cast<size_t>(L.m) * (d + 3);
     JOFC_CUDA(c->rho_part.ensure((static_cast<size_t>(c->epi_grid) + 1) * K));
     ep.rho = 1;
+    ep.rho_split = c->nccl_comm ? 1 : 0;
     ep.rho_partials = c->rho_part.p;
     ep.sumsq = c->sumsq.p;
     ep.within = c->consts.p + 3 * mm;
@@ -517,8 +528,16 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   auto exchange_pre = [&]() -> int {
     return nccl_x ? nccl_reduce(c, exchange(c), fid_slot(c)) : JOFC_OK;
   };
+  // (identity-form fidelity: the ranks' folded sums ride in the all-gather
+  // group, then the decision kernel)
+  const size_t rho_k = 1 + static_cast<size_t>(L.m) * (d + 3);
+  double* rho_sums = ep.rho_split ? ep.rho_partials + static_cast<size_t>(c->epi_grid) * rho_k
+                                  : nullptr;
   auto exchange_post = [&](size_t t) -> int {
-    return nccl_x ? nccl_gather(c, xbuf(c, static_cast<int>((t + 1) & 1))) : JOFC_OK;
+    if (!nccl_x) return JOFC_OK;
+    JOFC_TRY(nccl_gather(c, xbuf(c, static_cast<int>((t + 1) & 1)), rho_sums, rho_k));
+    if (rho_sums) JOFC_TRY(rho_decide_for_d(c, ep));
+    return JOFC_OK;
   };
   if (early_stop && !c->stop_flag) {
     JOFC_CUDA(cudaMallocHost(&c->stop_flag, 2 * sizeof(int)));
@@ -611,7 +630,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
     }
     for (size_t ch = 0; ch * per_graph <= max_it; ++ch) {
       JOFC_CUDA(cudaGraphLaunch(it->second, c->stream));
-      c->launches += (fused ? 1 : 2) * per_graph;  // (our kernels; NCCL's not counted)
+      c->launches += (fused ? 1 : rho_sums ? 3 : 2) * per_graph;  // (ours; NCCL's not counted)
       if (early_stop) {
         bool stop = false;
         JOFC_TRY(chunk_done(ch, &stop));
@@ -658,6 +677,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
       ++c->launches;
     }
     JOFC_TRY(exchange_post(t));
+    if (rho_sums) ++c->launches;
   }
   if (events) JOFC_CUDA(cudaEventRecord((*events)[max_it + 1], c->stream));
   c->max_it_enqueued = max_it;

@@ -189,7 +189,8 @@ def _nccl_worker(rank, world, port, payload, out):
     # modality's row chunks (gloo has no reduce_scatter: all-reduce + own
     # chunk, the same values), a fidelity all-reduce, the W^-1 mix of the OWN
     # chunk's objects only, commensurability of the replicated X_t over all
-    # objects (every rank, same order), an all-gather of X_{t+1} row chunks
+    # objects (every rank, same order), an all-gather of X_{t+1} row chunks;
+    # and the identity-form sigma from the all-reduced own-row sums
     import torch
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -213,12 +214,44 @@ def _nccl_worker(rank, world, port, payload, out):
     xn = np.zeros((m, n_pad, d))
     xn[:, lo:hi] = np.einsum("jl,lic->jic", coef, Pd[:, lo:hi])
     com = sum(cross[a, b] * np.sum((x[a] - x[b]) ** 2) for a in range(m) for b in range(a + 1, m))
+    # identity-form fidelity (csrc/jofc_kernels.cuh rho_fold / rho_decide):
+    # each rank folds, over ITS rows only, the commensurability and per
+    # modality R = x_i . P_i (reduced P rows), Q = |x_i - x_0|^2, its shard's
+    # A = sum of its stored delta^2, C = x_i - x_0; the vector rides in the
+    # all-gather group as one all-reduce
+    A = shard_sumsq(delta, m, n, rank, world)
+    vec = [sum(cross[a, b] * np.sum((x[a, lo:hi] - x[b, lo:hi]) ** 2)
+               for a in range(m) for b in range(a + 1, m))]
+    for l in range(m):
+        dx = x[l, lo:hi] - x[l, 0]
+        vec += [float(np.sum(x[l, lo:hi] * Pd[l, lo:hi])), float(np.sum(dx * dx)), A[l]]
+        vec += list(dx.sum(0))
     for l in range(m):  # all-gather of X_{t+1} row chunks
         parts = [torch.zeros(chunk, d, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(xn[l, own].copy()))
         xn[l] = torch.cat(parts).numpy()
-    out[rank] = (xn[:, :n], float(f[0]) + com)
+    v = torch.tensor(vec, dtype=torch.float64)
+    dist.all_reduce(v)
+    v = v.numpy()
+    sig_rho = v[0]
+    for l in range(m):
+        R, Q, Al = v[1 + l * (d + 3): 4 + l * (d + 3)]
+        C = v[4 + l * (d + 3): 1 + (l + 1) * (d + 3)]
+        sig_rho += within[l] * (Al + (n * Q - C @ C) - 2 * R)
+    out[rank] = (xn[:, :n], float(f[0]) + com, sig_rho)
     dist.destroy_process_group()
+
+
+def shard_sumsq(delta, m, n, rank, world):
+    """A_l over one shard's blocks (jofc_modality_sumsq_kernel)."""
+    A = np.zeros(m)
+    for l, B, J in layout.blocks(m, n, rank, world):
+        r0, c0 = B * layout.ROWS, J * layout.COLS
+        for i in range(r0, min(r0 + layout.ROWS, n)):
+            j0, j1 = max(c0, i + 1), min(c0 + layout.COLS, n)
+            if j1 > j0:
+                A[l] += np.sum(delta[l, i, j0:j1] ** 2)
+    return A
 
 
 @pytest.mark.parametrize("world", [2, 4])
@@ -240,8 +273,9 @@ def test_nccl_native_decomposition_gloo_matches_oracle(world):
     ref_step = P.guttman_step_fast(delta, spec, x)
     ref_stress = P.raw_stress(delta, spec, x)
     for r in range(world):
-        xn, sigma = out[r]
+        xn, sigma, sigma_rho = out[r]
         assert np.linalg.norm(xn - ref_step) / np.linalg.norm(ref_step) < 1e-12
         assert abs(sigma - ref_stress) / ref_stress < 1e-12
+        assert abs(sigma_rho - ref_stress) / ref_stress < 1e-12
     for r in range(1, world):  # replicated X and stop state on every rank
-        assert np.array_equal(out[r][0], out[0][0]) and out[r][1] == out[0][1]
+        assert np.array_equal(out[r][0], out[0][0]) and out[r][1:] == out[0][1:]
