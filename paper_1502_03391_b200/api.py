@@ -310,12 +310,14 @@ class Device:
     # SPMD id broadcast / init sequence
     @staticmethod
     def nccl_unique_id():
+        _process_nccl()
         buf = C.create_string_buffer(128)
         check(_capi.load().jofc_nccl_unique_id(buf))
         return buf.raw
 
     @staticmethod
     def nccl_version():
+        _process_nccl()
         v = C.c_int()
         check(_capi.load().jofc_nccl_version(C.byref(v)))
         return int(v.value)
@@ -323,6 +325,7 @@ class Device:
     def nccl_init(self, uid, rank, world):
         if len(uid) != 128:
             raise InvalidArgument("NCCL exchange: the unique id is 128 bytes")
+        _process_nccl()
         check(self.lib.jofc_nccl_init(self.h, uid, int(rank), int(world)))
 
     def nccl_release(self):
@@ -401,6 +404,17 @@ class Device:
 
 
 _default_devices = {}
+
+
+def _process_nccl():
+    """Load torch (when installed) before the C library resolves NCCL: its
+    bundled libnccl.so.2 is then the process's one NCCL (csrc/capi_nccl.cu
+    reuses an already-loaded copy), instead of an older system copy that
+    would later satisfy torch's own libnccl.so.2 dependency and break it."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
 
 
 def default_device(device=0):

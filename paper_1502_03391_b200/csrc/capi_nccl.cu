@@ -37,6 +37,7 @@
 #include <nccl.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -80,8 +81,14 @@ const NcclApi& nccl() {
   static std::once_flag once;
   std::call_once(once, [] {
     // a copy already in the process first (one NCCL instance per process)
+    // then JOFC_NCCL_LIB, then the loader's libnccl.so.2.  (A process that
+    // will also use torch should import torch first: once loaded here, a
+    // libnccl.so.2 satisfies torch's own dependency by soname, and an older
+    // system copy lacks symbols torch's build needs -- api.py does that.)
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    const char* env = std::getenv("JOFC_NCCL_LIB");
+    if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) {
       api.error = std::string("libnccl.so.2 not loadable: ") + dlerror();
       return;

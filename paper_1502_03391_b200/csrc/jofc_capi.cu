@@ -224,14 +224,17 @@ int setup_for(jofc_ctx* c) {
 
 template <int D>
 int launch_epi(jofc_ctx* c, const EpiParams& ep) {
-  jofc_epilogue_kernel<D><<<c->epi_grid, 256, 0, c->stream>>>(ep);
+  if (ep.rho && ep.m <= kWideMaxM)
+    jofc_epilogue_wide_kernel<D><<<c->rho_grid, kWideThreads, 0, c->stream>>>(ep);
+  else
+    jofc_epilogue_kernel<D><<<c->epi_grid, kEpiThreads, 0, c->stream>>>(ep);
   JOFC_CUDA(cudaGetLastError());
   return JOFC_OK;
 }
 
 template <int D>
 int launch_rho_decide(jofc_ctx* c, const EpiParams& ep) {
-  jofc_rho_decide_kernel<D><<<1, 32, 0, c->stream>>>(ep, static_cast<unsigned>(c->epi_grid));
+  jofc_rho_decide_kernel<D><<<1, 32, 0, c->stream>>>(ep, static_cast<unsigned>(c->rho_grid));
   JOFC_CUDA(cudaGetLastError());
   return JOFC_OK;
 }
@@ -345,7 +348,7 @@ int alloc_solve_state(jofc_ctx* c, size_t d, size_t max_it) {
     }
   }
   c->pass_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(c->num_sms, L.local())));
-  c->epi_grid = static_cast<int>((L.n + 255) / 256);
+  c->epi_grid = static_cast<int>((L.n + kEpiThreads - 1) / kEpiThreads);
   JOFC_CUDA(c->fid_part.ensure(2 * static_cast<size_t>(c->pass_grid)));
   JOFC_TRY(pass_bounds(c));
   // (the persistent kernel keeps one commensurability partial per pass CTA)
@@ -490,7 +493,12 @@ int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t 
   if (rho_enabled() && c->fidelity_form == JOFC_FIDELITY_AUTO &&
       (c->world == 1 || c->nccl_comm) && !c->peer.active && !pp.fuse_epilogue && c->sumsq.p) {
     const size_t K = 1 + static_cast<size_t>(L.m) * (d + 3);
-    JOFC_CUDA(c->rho_part.ensure((static_cast<size_t>(c->epi_grid) + 1) * K));
+    const long long wide_objs = static_cast<long long>(kWideThreads / 32 / L.m) * 32;
+    c->rho_grid = L.m <= kWideMaxM
+                      ? static_cast<int>(std::min<long long>(c->num_sms,
+                                                             (L.n + wide_objs - 1) / wide_objs))
+                      : c->epi_grid;
+    JOFC_CUDA(c->rho_part.ensure((static_cast<size_t>(c->rho_grid) + 1) * K));
     ep.rho = 1;
     ep.rho_split = c->nccl_comm ? 1 : 0;
     ep.rho_partials = c->rho_part.p;
@@ -531,7 +539,7 @@ int enqueue_solve(jofc_ctx* c, const jofc_weights* spec, size_t d, const double*
   // (identity-form fidelity: the ranks' folded sums ride in the all-gather
   // group, then the decision kernel)
   const size_t rho_k = 1 + static_cast<size_t>(L.m) * (d + 3);
-  double* rho_sums = ep.rho_split ? ep.rho_partials + static_cast<size_t>(c->epi_grid) * rho_k
+  double* rho_sums = ep.rho_split ? ep.rho_partials + static_cast<size_t>(c->rho_grid) * rho_k
                                   : nullptr;
   auto exchange_post = [&](size_t t) -> int {
     if (!nccl_x) return JOFC_OK;
