@@ -30,7 +30,7 @@ $(PKG)/libjofc_gpu.so: $(GPU_SRC) $(GPU_HDR)
 # kernel experiments: `make exp EXP=-DJOFC_EXP_...` builds the same C ABI with an
 # experimental switch into libjofc_gpu_exp.so (selected with JOFC_GPU_LIB)
 exp:
-	$(NVCC) $(NVFLAGS) $(EXP) -shared -o $(PKG)/libjofc_gpu_exp.so $(GPU_SRC) -lgomp -ldl
+	$(NVCC) $(NVFLAGS) $(EXP) -shared -o $(PKG)/libjofc_gpu_$(or $(EXPNAME),exp).so $(GPU_SRC) -lgomp -ldl
 
 $(PKG)/libjofc.so: $(DROPIN_SRC) $(DROPIN_HDR) $(PKG)/libjofc_gpu.so
 	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -I$(CSRC) -o $@ $(DROPIN_SRC) \

@@ -683,7 +683,9 @@ def run_oos(args):
                      "peak_source": f"measured here: L2-resident reads of a {bytes_per_it / 1e6:.0f} "
                                     f"MB buffer (libjofc_probe.so jofc_probe_l2_read)",
                      "per": "rank 0's GPU (its share of the delta rows)",
-                     "kernel": "jofc_oos_pass_kernel + jofc_oos_update_kernel (one update)",
+                     "kernel": ("jofc_oos_solve_kernel: the whole batch solve in one launch "
+                                "(+ jofc_oos_permute_kernel once per batch); update_us = step "
+                                "time / updates"),
                      "update_us": round(it_s * 1e6, 2),
                      "fp64": ({"algorithmic_flops_per_entry": 5 * d + 7,
                                "achieved_tflops": round(entries * (5 * d + 7) / it_s / 1e12, 2),

@@ -233,6 +233,7 @@ struct jofc_ctx {
   // oos state
   DevBuf<double> oos_x, oos_delta, oos_y0, oos_y1, oos_part, oos_trace;
   DevBuf<double> oos_delta_t;  // [j][point group][n][32] (v2 pass)
+  DevBuf<double> oos_delta_p;  // ring order of the persistent solve (jofc_oos_permute_kernel)
   DevBuf<OosPoint> oos_st;
   DevBuf<unsigned> oos_done;
   // streaming ingest staging

@@ -765,7 +765,8 @@ int jofc_ctx_destroy(jofc_ctx* c) {
   nccl_release(c);
   for (DevBuf<double>* b : {&c->delta, &c->x0, &c->x1, &c->P, &c->fid_part, &c->com_part,
                             &c->trace, &c->consts, &c->oos_x, &c->oos_delta, &c->oos_y0,
-                            &c->oos_y1, &c->oos_part, &c->oos_trace, &c->oos_delta_t})
+                            &c->oos_y1, &c->oos_part, &c->oos_trace, &c->oos_delta_t,
+                            &c->oos_delta_p})
     b->release();
   c->ctrl.release();
   c->up_bad.release();
@@ -1130,10 +1131,12 @@ namespace {
 // (jofc_oos_step_kernel, default); 1 = pass (warp per point, lanes over rows)
 // + update kernel, the round-2 pair; 2 = the lanes-over-points pass on the
 // transposed delta + update kernel.  JOFC_OOS_KERNEL=1/2 for comparisons.
+// 4 (default) = the persistent solve (jofc_oos_solve_kernel: one launch per
+// batch) where its shared-memory plan fits, else 3.
 int oos_kernel_version() {
   static const int v = [] {
     const char* e = std::getenv("JOFC_OOS_KERNEL");
-    return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 3;
+    return (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 4;
   }();
   return v;
 }
@@ -1151,7 +1154,7 @@ long long oos_splits() {
 template <int D>
 int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
   const bool v2 = oos_kernel_version() == 2;
-  const bool fused = oos_kernel_version() == 3;
+  const bool fused = oos_kernel_version() >= 3;  // (4: the persistent solve did not apply)
   // v1: 4 slices of the in-sample range (measured best at C5 among 2..16)
   const dim3 pg((op.k + kOosWarps - 1) / kOosWarps, op.m,
                 static_cast<unsigned>(std::min<long long>(oos_splits(), std::max<long long>(1, op.n / 256))));
@@ -1266,6 +1269,104 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
   return JOFC_OK;
 }
 
+// The persistent solve (jofc_oos_solve_kernel): one CTA per SM, each owning a
+// contiguous range of <= G points for the whole solve.  Returns 1 (nothing
+// launched) when the batch does not fit the kernel's shared-memory plan: the
+// caller falls back to the per-update kernels.
+constexpr int kSmemOptin = 231424;  // 227 KB per CTA less the 1 KB the driver reserves
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+template <int D>
+int oos_launch_persistent(jofc_ctx* c, const OosParams& op) {
+  constexpr int Q = oosp_q<D>();
+  constexpr int V = D + 2;
+  const int m = op.m, k = op.k;
+  static const long long rows_env = [] {  // experiments: rows per chunk
+    const char* e = std::getenv("JOFC_OOSP_ROWS");
+    return e ? std::atoll(e) : 0LL;
+  }();
+  static const long long g_env = [] {  // experiments: points per CTA
+    const char* e = std::getenv("JOFC_OOSP_G");
+    return e ? std::atoll(e) : 0LL;
+  }();
+  JOFC_CUDA(ensure_smem_attr(jofc_oos_solve_kernel<D>, kSmemOptin, c->device));
+  int G = static_cast<int>(std::min<long long>((k + c->num_sms - 1) / c->num_sms, kOospConsumers * Q));
+  if (g_env > 0) G = static_cast<int>(std::min<long long>(g_env, kOospConsumers * Q));
+  int S = 1;  // slots: the smallest divisor of the consumer warps holding G points
+  while (S * Q < G || kOospConsumers % S) ++S;
+  OospParams pp{};
+  // fixed part: part, y, warp sums, previous stresses, sums of X, done flags
+  const size_t fixed_bytes = static_cast<size_t>(m) * G * V * 8 + 2ull * G * m * D * 8 +
+                             static_cast<size_t>(kOospConsumers) * Q * V * 8 + static_cast<size_t>(G) * 8 +
+                             static_cast<size_t>(m) * D * 8 + static_cast<size_t>(G) * 4 + 64;
+  int R = 0, stages = 0;
+  const int lanes_per_slot = 32 * (kOospConsumers / S);  // R a multiple: every lane the same rows
+  for (int r0 : {512, 256, 128, 64}) {
+    if (rows_env && r0 != rows_env) continue;
+    const int r = std::max(lanes_per_slot, r0 / lanes_per_slot * lanes_per_slot);
+    const size_t stage = (static_cast<size_t>(G) * r + static_cast<size_t>(r) * D + 2) * 8;
+    const long long room = static_cast<long long>(kSmemOptin) - 128 - static_cast<long long>(fixed_bytes);
+    const int st = static_cast<int>(std::min<long long>(kOospMaxStages, room / static_cast<long long>(stage)));
+    if (st >= 4 || (st >= 2 && r0 == 64) || (rows_env && st >= 2)) {
+      R = r;
+      stages = st;
+      break;
+    }
+  }
+  if (R == 0) return 1;
+  pp.x = op.x;
+  pp.deltas = op.deltas;
+  pp.ystart = op.y0;
+  pp.yout0 = op.y0;
+  pp.yout1 = op.y1;
+  pp.traces = op.traces;
+  pp.st = op.st;
+  pp.k = k;
+  pp.m = m;
+  pp.n = op.n;
+  pp.w = op.w;
+  pp.eps = op.eps;
+  pp.term_count = op.term_count;
+  pp.max_it = op.max_it;
+  pp.fixed = op.fixed;
+  pp.G = G;
+  pp.S = S;
+  pp.ncta = (k + G - 1) / G;
+  pp.R = R;
+  pp.stages = stages;
+  pp.nch = static_cast<int>((op.n + R - 1) / R);
+  pp.stage_doubles = static_cast<unsigned>(static_cast<size_t>(G) * R + static_cast<size_t>(R) * D + 2);
+  // delta in ring order (once per batch)
+  const size_t nperm = static_cast<size_t>(pp.ncta) * m * pp.nch * G * R;
+  JOFC_CUDA(c->oos_delta_p.ensure(nperm));
+  pp.dperm = c->oos_delta_p.p;
+  jofc_oos_permute_kernel<<<static_cast<unsigned>(nperm / R), 256, 0, c->stream>>>(
+      op.deltas, c->oos_delta_p.p, k, m, op.n, pp.ncta, G, R, pp.nch);
+  JOFC_CUDA(cudaGetLastError());
+  ++c->launches;
+  size_t o = 128;
+  pp.off_ring = static_cast<unsigned>(o);
+  o += static_cast<size_t>(stages) * pp.stage_doubles * 8;
+  pp.off_part = static_cast<unsigned>(o);
+  o += static_cast<size_t>(m) * G * V * 8;
+  pp.off_y = static_cast<unsigned>(o);
+  o += 2ull * G * m * D * 8;
+  pp.off_red = static_cast<unsigned>(o);
+  o += static_cast<size_t>(kOospConsumers) * Q * V * 8;
+  pp.off_misc = static_cast<unsigned>(o);
+  o += static_cast<size_t>(G) * 8 + static_cast<size_t>(m) * D * 8 + static_cast<size_t>(G) * 4;
+  const size_t bytes = align_up(o, 16);
+  if (bytes > static_cast<size_t>(kSmemOptin)) return 1;
+  if (std::getenv("JOFC_OOSP_DEBUG"))
+    std::fprintf(stderr, "oosp: k %d m %d n %lld D %d: G %d S %d R %d stages %d ncta %d nch %d smem %zu\n",
+                 k, m, op.n, D, G, S, R, stages, pp.ncta, pp.nch, bytes);
+  jofc_oos_solve_kernel<D><<<pp.ncta, kOospThreads, bytes, c->stream>>>(pp);
+  JOFC_CUDA(cudaGetLastError());
+  ++c->launches;
+  return JOFC_OK;
+}
+
 int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x,
             const double* deltas, double w, const double* y0, double eps, size_t max_it,
             int fixed, double* y_out, double* traces, size_t* iterations, double* stress0) {
@@ -1278,7 +1379,7 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
     return set_error(JOFC_EINVAL, "dim %zu unsupported (1..%d)", d, kMaxD);
   JOFC_CUDA(cudaSetDevice(c->device));
   JOFC_CUDA(c->oos_x.ensure(m * n * d + 4));  // + slack: chunk copies round up to 16 bytes
-  JOFC_CUDA(c->oos_delta.ensure(k * m * n));
+  JOFC_CUDA(c->oos_delta.ensure(k * m * n + 2));  // + slack: segment copies round up to 16 bytes
   const int groups = static_cast<int>((k + 31) / 32);
   if (oos_kernel_version() == 2)
     JOFC_CUDA(c->oos_delta_t.ensure(static_cast<size_t>(groups) * 32 * m * n));
@@ -1328,8 +1429,23 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
   op.term_count = static_cast<double>(m * n) + 0.5 * static_cast<double>(m * (m - 1));
   op.max_it = static_cast<int>(max_it);
   op.fixed = fixed;
-  int rc;
-  switch (d) {
+  int rc = 1;
+  if (oos_kernel_version() == 4) {
+    switch (d) {
+      case 1: rc = oos_launch_persistent<1>(c, op); break;
+      case 2: rc = oos_launch_persistent<2>(c, op); break;
+      case 3: rc = oos_launch_persistent<3>(c, op); break;
+      case 4: rc = oos_launch_persistent<4>(c, op); break;
+      case 5: rc = oos_launch_persistent<5>(c, op); break;
+      case 6: rc = oos_launch_persistent<6>(c, op); break;
+      case 7: rc = oos_launch_persistent<7>(c, op); break;
+      case 8: rc = oos_launch_persistent<8>(c, op); break;
+      case 9: rc = oos_launch_persistent<9>(c, op); break;
+      default: rc = oos_launch_persistent<10>(c, op); break;
+    }
+    if (rc != JOFC_OK && rc != 1) return rc;
+  }
+  if (rc == 1) switch (d) {
     case 1: rc = oos_launch<1>(c, op, static_cast<int>(max_it)); break;
     case 2: rc = oos_launch<2>(c, op, static_cast<int>(max_it)); break;
     case 3: rc = oos_launch<3>(c, op, static_cast<int>(max_it)); break;

@@ -609,4 +609,419 @@ __global__ void __launch_bounds__(kOosWarps * 32) jofc_oos_step_kernel(const Oos
   }
 }
 
+// ------------------------------------------------------ persistent solve
+// The whole out-of-sample batch solve in ONE launch.  Points are independent
+// (proj/src/oos.cpp:180-229 runs one oos_embed per point), so each CTA (one
+// per SM) owns a contiguous range of at most G points for every iteration --
+// no grid-wide synchronisation, no per-iteration launches.  A producer warp
+// streams chunks of R in-sample rows through a TMA ring: for modality l, the
+// G points' delta rows (one bulk copy: the batch's delta is permuted into
+// ring order once, jofc_oos_permute_kernel) and the rows of X^(l) (one
+// more), in the order (iteration, modality, chunk); delta and X do not
+// depend on y, so the ring runs on across the update steps.  8 consumer
+// warps, per iteration:
+//   pass    lanes over rows; a lane keeps Q points of its warp's slot in
+//           registers (register u holds point u ^ pi(lane): the fold below is
+//           a select-free reduce-scatter) and, per row and point:
+//           r = [dist != 0] delta / dist, psi += r, fidelity += (delta -
+//           dist)^2, xi' += r x_k (xi = sum_k x_k - xi', one FP64 operation
+//           per entry less than (1 - r) x_k);
+//   fold    per modality: lanes -> warp (log2 Q reduce-scatter levels + a
+//           butterfly), warps -> point in a fixed order, into part[l][q];
+//   update  thread q: sigma_t (proj/src/oos.cpp:50-70), the stop rule
+//           (:221-226) and y_{t+1} of every modality (:98-111); the trace,
+//           the state and the final y go to global memory.
+// Ring protocol: full[s] (TMA completion, waited by the consumers), empty[s]
+// (one release-arrive per consumer warp, acquired by the producer before
+// its fence.proxy.async and the bulk copies that overwrite the stage).
+// (9 warps: 168 registers per thread, 4 points per lane at d <= 4.  Measured
+// per C5 update (batch of 1000, `scripts/gpu_oosp_ab.sh`): 8 consumers x 4
+// points 24.7 us; 16 x 2 26.5 us; 12 x 2 or 12 x 4 (128 registers) 27-29 us;
+// 24 x 2 (72 registers) 35.7 us; two rows per lane in flight: slower)
+#ifndef JOFC_OOSP_CONSUMERS
+#define JOFC_OOSP_CONSUMERS 8
+#endif
+constexpr int kOospConsumers = JOFC_OOSP_CONSUMERS;     // consumer warps
+constexpr int kOospThreads = (kOospConsumers + 1) * 32;  // + the producer warp
+constexpr int kOospMaxStages = 6;
+#ifndef JOFC_OOSP_UNROLL
+#define JOFC_OOSP_UNROLL 1
+#endif
+constexpr int kOospUnroll = JOFC_OOSP_UNROLL;  // rows per lane in flight (experiments)
+
+// Points per warp slot (a power of 2): Q (D + 2) accumulators and Q D
+// coordinates of y per lane (<= 168 registers at 9 warps).
+template <int D>
+__host__ __device__ constexpr int oosp_q() {
+#ifdef JOFC_OOSP_Q
+  return D <= 4 ? JOFC_OOSP_Q : 1;  // (experiments)
+#else
+  return D <= 4 ? 4 : (D <= 8 ? 2 : 1);
+#endif
+}
+
+struct OospParams {
+  const double* x;       // m x n x D (the frozen in-sample configuration)
+  const double* deltas;  // k x m x n
+  const double* ystart;  // k x m x D
+  double* yout0;         // final y of a point -> buffer (iterations & 1)
+  double* yout1;
+  double* traces;        // k x (max_it + 1)
+  OosPoint* st;
+  int k, m;
+  long long n;
+  double w, eps, term_count;
+  int max_it, fixed;
+  int ncta;    // CTA b owns points [b k / ncta, (b + 1) k / ncta)
+  int G;       // max points per CTA
+  int S;       // point slots (divides kOospConsumers): point q -> slot q % S, register q / S
+  int R;       // rows per chunk (even)
+  int stages;  // ring depth (<= kOospMaxStages)
+  int nch;     // chunks per modality pass, ceil(n / R)
+  unsigned stage_doubles;  // G R delta + (R D + 2) X
+  // delta rows in ring order (jofc_oos_permute_kernel): for CTA b, modality
+  // l, chunk ch one contiguous G x R block (point-major, zero padded)
+  const double* dperm;
+  // dynamic shared-memory layout (byte offsets from the base)
+  unsigned off_ring, off_part, off_y, off_red, off_misc;
+};
+
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kOospConsumers * 32) : "memory");
+}
+
+// Consumer-wide OR (named barrier 1, the producer warp excluded).
+__device__ __forceinline__ int consumers_or(int v) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.s32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, 1, %2, p;\n\t"
+      "selp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(v), "n"(kOospConsumers * 32)
+      : "memory");
+  return r;
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// delta (k x m x n) -> the persistent solve's ring order: block
+// (b, l, ch) = rows [ch R, ch R + R) of modality l for CTA b's G point slots,
+// point-major, zeros past n and past the CTA's points.  Once per batch.
+static __global__ void __launch_bounds__(256) jofc_oos_permute_kernel(const double* __restrict__ d,
+                                                                      double* __restrict__ out,
+                                                                      int k, int m, long long n,
+                                                                      int ncta, int G, int R,
+                                                                      int nch) {
+  // CTA = one segment (b, l, ch, q): R consecutive doubles of the output
+  const long long seg = blockIdx.x;
+  const int q = static_cast<int>(seg % G);
+  long long rest = seg / G;
+  const int ch = static_cast<int>(rest % nch);
+  rest /= nch;
+  const int l = static_cast<int>(rest % m);
+  const int b = static_cast<int>(rest / m);
+  const int p_lo = static_cast<int>(static_cast<long long>(b) * k / ncta);
+  const int g = static_cast<int>(static_cast<long long>(b + 1) * k / ncta) - p_lo;
+  const long long row0 = static_cast<long long>(ch) * R;
+  const double* src = d + (static_cast<long long>(p_lo + q) * m + l) * n + row0;
+  double* dst = out + seg * R;
+  const long long rows = (q < g) ? min(static_cast<long long>(R), n - row0) : 0;
+  for (int r = threadIdx.x; r < R; r += blockDim.x) dst[r] = (r < rows) ? __ldcs(src + r) : 0.0;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kOospThreads, 1) jofc_oos_solve_kernel(const OospParams p) {
+  constexpr int Q = oosp_q<D>();
+  constexpr int V = D + 2;  // per (point, modality): psi, fidelity, xi[D]
+  constexpr int kLanesPerPt = 32 / Q;  // lanes that end up holding one point's sums
+  extern __shared__ __align__(128) unsigned char oosp_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(oosp_smem);       // kOospMaxStages
+  uint64_t* empty = full + kOospMaxStages;                         // kOospMaxStages
+  volatile int* stop = reinterpret_cast<volatile int*>(empty + kOospMaxStages);
+  volatile long long* consumed = reinterpret_cast<volatile long long*>(oosp_smem + 112);
+  double* ring = reinterpret_cast<double*>(oosp_smem + p.off_ring);
+  double* part = reinterpret_cast<double*>(oosp_smem + p.off_part);  // m x G x V
+  double* ybuf = reinterpret_cast<double*>(oosp_smem + p.off_y);     // 2 x G x m x D
+  double* sred = reinterpret_cast<double*>(oosp_smem + p.off_red);   // warps x Q x V
+  double* prev = reinterpret_cast<double*>(oosp_smem + p.off_misc);  // G: sigma_{t-1}
+  double* sx = prev + p.G;                                           // m x D: sum_k x_k
+  int* pdone = reinterpret_cast<int*>(sx + p.m * D);                 // G
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = p.m, kSt = p.stages;
+  const int p_lo = static_cast<int>(static_cast<long long>(blockIdx.x) * p.k / p.ncta);
+  const int g = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.k / p.ncta) - p_lo;
+  const long long n = p.n;
+  const int R = p.R, nch = p.nch;
+  const long long total_chunks = static_cast<long long>(p.max_it + 1) * m * nch;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSt; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kOospConsumers);
+    }
+    *stop = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == kOospConsumers) {
+    // ---- producer: chunk gc (order: iteration, modality, rows) into stage
+    // gc % kSt once the consumers released its previous use; delta segments
+    // start at their first row rounded down to an even index (16-byte
+    // aligned bulk copies)
+    if (lane != 0) return;
+    long long gc = 0;
+    int stg = 0;
+    uint32_t ph = 0;  // (gc / kSt) & 1
+    for (int l = 0, ch = 0; gc < total_chunks; ++gc) {
+      if (gc >= kSt) {
+        bool ok;
+        // (the stage's previous use, chunk gc - kSt, completed phase ph ^ 1)
+        while (!(ok = mbar_try_wait(&empty[stg], ph ^ 1u)) && !*stop) {
+        }
+        if (!ok) break;  // the solve ended: nothing more is consumed
+        fence_proxy_async_smem();
+      }
+      // two bulk copies per chunk: the TMA engine's cost is per copy (one
+      // 4 KB copy per point measured ~0.9 us per chunk whatever its size)
+      const long long k0 = static_cast<long long>(ch) * R;
+      const int rows = static_cast<int>(min(static_cast<long long>(R), n - k0));
+      double* base = ring + static_cast<long long>(stg) * p.stage_doubles;
+      const long long xfirst = (static_cast<long long>(l) * n + k0) * D;
+      const uint32_t xbytes = static_cast<uint32_t>((((xfirst & 1) + rows * D) * 8 + 15) & ~15LL);
+      const uint32_t dbytes = static_cast<uint32_t>(p.G) * R * 8;
+      mbar_expect_tx(&full[stg], xbytes + dbytes);
+      bulk_g2s(base, p.dperm + ((static_cast<long long>(blockIdx.x) * m + l) * nch + ch) * p.G * R,
+               dbytes, &full[stg]);
+      bulk_g2s(base + static_cast<long long>(p.G) * R, p.x + (xfirst & ~1LL), xbytes, &full[stg]);
+      if (++stg == kSt) {
+        stg = 0;
+        ph ^= 1u;
+      }
+      if (++ch == nch) {
+        ch = 0;
+        if (++l == m) l = 0;
+      }
+    }
+    // drain: every chunk issued but never consumed must land before the CTA
+    // (and its shared memory) goes away
+    while (!*stop) {
+    }
+    __threadfence_block();
+    for (long long q = *consumed; q < gc; ++q)
+      mbar_wait(&full[q % kSt], static_cast<uint32_t>((q / kSt) & 1));
+    return;
+  }
+
+  // ---- consumers
+  const int S = p.S, WS = kOospConsumers / S;
+  const int slot = warp % S, wi = warp / S;
+  const int pi = lane / kLanesPerPt;  // this lane's point permutation (0 .. Q-1)
+  constexpr int kT = kOospConsumers * 32;
+  for (int e = threadIdx.x; e < g * m * D; e += kT)
+    ybuf[e] = p.ystart[static_cast<long long>(p_lo) * m * D + e];
+  for (int q = threadIdx.x; q < g; q += kT) pdone[q] = 0;
+  // sum_k x_k of every modality (fixed order; warp l sums modality l, ...)
+  for (int l = warp; l < m; l += kOospConsumers) {
+    double a[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) a[c] = 0.0;
+    const double* xl = p.x + static_cast<long long>(l) * n * D;
+    for (long long r = lane; r < n; r += 32)
+#pragma unroll
+      for (int c = 0; c < D; ++c) a[c] += xl[r * D + c];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a[c] += __shfl_xor_sync(0xffffffffu, a[c], o);
+      if (lane == 0) sx[l * D + c] = a[c];
+    }
+  }
+  consumers_sync();
+
+  const double nn = static_cast<double>(n);
+  const double mw = static_cast<double>(m) * p.w;
+  const double direct = 1.0 / (nn + mw);
+  const double spread = p.w / (nn * (nn + mw));
+  long long gc = 0;  // chunks consumed
+  int stg = 0;
+  uint32_t ph = 0;
+  for (int t = 0;; ++t) {
+    for (int l = 0; l < m; ++l) {
+      // ---- pass of modality l for y_t: register u holds point
+      // q_u = slot + S (u ^ pi) (points past g or finished compute on a
+      // clamped segment and are never read)
+      double yv[Q][D], acc[Q][V];
+      int seg[Q];  // a point's delta segment in a stage (doubles; 32-bit offsets)
+#pragma unroll
+      for (int u = 0; u < Q; ++u) {
+        const int q = min(slot + S * (u ^ pi), g - 1);
+        seg[u] = q * R;
+#pragma unroll
+        for (int c = 0; c < D; ++c) yv[u][c] = ybuf[((t & 1) * p.G + q) * m * D + l * D + c];
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[u][v] = 0.0;
+      }
+      const int xpar = static_cast<int>((static_cast<long long>(l) * n * D) & 1);
+      for (int ch = 0; ch < nch; ++ch, ++gc) {
+        const int rows = static_cast<int>(min(static_cast<long long>(R), n - static_cast<long long>(ch) * R));
+        mbar_wait(&full[stg], ph);
+        const double* base = ring + static_cast<long long>(stg) * p.stage_doubles;
+        const double* xk0 = base + static_cast<long long>(p.G) * R + ((xpar + ch * R * D) & 1);
+#ifdef JOFC_OOSP_DIAG  // timing experiment: streaming only (results wrong)
+        if (rows > 0) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stg]);
+          if (++stg == kSt) {
+            stg = 0;
+            ph ^= 1u;
+          }
+          continue;
+        }
+#endif
+#pragma unroll kOospUnroll
+        for (int r = lane + 32 * wi; r < rows; r += 32 * WS) {
+          double xk[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) xk[c] = xk0[r * D + c];
+#pragma unroll
+          for (int u = 0; u < Q; ++u) {
+            const double dv = base[seg[u] + r];
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              const double df = xk[c] - yv[u][c];
+              s = (c == 0) ? df * df : fma(df, df, s);
+            }
+            // dist == 0 guard (proj/src/oos.cpp:88) as an integer test of the
+            // high word (s >= 0; s = 0 and the flushed denormals give 0)
+            const double y = rsqrt_nr(s);
+            const double inv = (__double2hiint(s) > 0) ? y : 0.0;
+            const double rt = dv * inv;
+            const double resid = fma(-s, inv, dv);
+            acc[u][0] += rt;
+            acc[u][1] = fma(resid, resid, acc[u][1]);
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[u][2 + c] = fma(rt, xk[c], acc[u][2 + c]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stg]);  // (release: this warp's reads of the stage)
+        if (++stg == kSt) {
+          stg = 0;
+          ph ^= 1u;
+        }
+      }
+      // ---- fold of modality l.  Reduce-scatter over the lane bits of pi:
+      // at the level of point bit h, register u (bit h clear) adds the
+      // partner's register u ^ h, which holds the same point.
+#pragma unroll
+      for (int h = Q / 2; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int u = 0; u < h; ++u)
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            acc[u][v] += __shfl_xor_sync(0xffffffffu, acc[u + h][v], h * kLanesPerPt);
+      }
+      // register 0 now holds point slot + S pi over the lanes sharing pi
+#pragma unroll
+      for (int o = kLanesPerPt / 2; o >= 1; o >>= 1)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[0][v] += __shfl_xor_sync(0xffffffffu, acc[0][v], o);
+      if ((lane & (kLanesPerPt - 1)) == 0)
+#pragma unroll
+        for (int v = 0; v < V; ++v) sred[(warp * Q + pi) * V + v] = acc[0][v];
+      consumers_sync();
+      for (int e = threadIdx.x; e < g * V; e += kT) {
+        const int q = e / V, v = e - q * V;
+        const int s = q % S, u = q / S;
+        double a = 0.0;
+        for (int w2 = 0; w2 < WS; ++w2) a += sred[((s + S * w2) * Q + u) * V + v];
+        // xi = sum_k x_k - sum_k r_k x_k
+        part[(l * p.G + q) * V + v] = (v >= 2) ? sx[l * D + v - 2] - a : a;
+      }
+      consumers_sync();
+    }
+    // ---- update step t of each point
+    int active = 0;
+    if (threadIdx.x < g && !pdone[threadIdx.x]) {
+      const int q = threadIdx.x;
+      const int pt = p_lo + q;
+      const double* yc = ybuf + ((t & 1) * p.G + q) * m * D;
+      double* yn = ybuf + (((t + 1) & 1) * p.G + q) * m * D;
+      double fid = 0.0, com = 0.0, xi_sum[D], psi_y[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xi_sum[c] = psi_y[c] = 0.0;
+      for (int l = 0; l < m; ++l) {
+        const double* pl = part + (l * p.G + q) * V;
+        fid += pl[1];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          xi_sum[c] += pl[2 + c];
+          psi_y[c] = fma(pl[0], yc[l * D + c], psi_y[c]);
+        }
+        for (int l2 = l + 1; l2 < m; ++l2) {
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            const double df = yc[l * D + c] - yc[l2 * D + c];
+            com = fma(df, df, com);
+          }
+        }
+      }
+      const double sigma = fid + p.w * com;
+      bool finished = false;
+      int status = 0;
+      if (!isfinite(sigma)) {
+        finished = true;
+        status = 2;
+      } else {
+        if (t >= 1 && !p.fixed && (prev[q] - sigma) / p.term_count < p.eps) finished = true;
+        if (t >= p.max_it) finished = true;
+      }
+      if (!finished)
+        for (int l = 0; l < m; ++l) {
+          const double* pl = part + (l * p.G + q) * V;
+#pragma unroll
+          for (int c = 0; c < D; ++c)
+            yn[l * D + c] = direct * (pl[2 + c] + pl[0] * yc[l * D + c]) +
+                            spread * (xi_sum[c] + psi_y[c]);
+        }
+      prev[q] = sigma;
+      if (p.traces) p.traces[static_cast<long long>(pt) * (p.max_it + 1) + t] = sigma;
+      if (finished) {
+        double* yo = ((t & 1) ? p.yout1 : p.yout0) + static_cast<long long>(pt) * m * D;
+        for (int e = 0; e < m * D; ++e) yo[e] = yc[e];
+        OosPoint s;
+        s.t = t;
+        s.done = 1;
+        s.iterations = t;
+        s.status = status;
+        p.st[pt] = s;
+        pdone[q] = 1;
+      }
+      active = !finished;
+    }
+    if (!consumers_or(active)) break;
+  }
+  // tell the producer where the solve ended (it drains what it issued past it)
+  if (threadIdx.x == 0) {
+    *consumed = gc;
+    __threadfence_block();
+    *stop = 1;
+  }
+}
+
 }  // namespace jofc_gpu
