@@ -163,6 +163,16 @@ def h2d_bytes_dense_upload(m, n, world, rank):
     return b
 
 
+def oos_traffic():
+    """L2 -> SM bytes per update of the persistent OOS solve (ncu; the roof is L2)."""
+    path = os.path.join(ROOT, "profiles", "oos_traffic_cfg5.json")
+    try:
+        with open(path) as f:
+            return json.load(f)["l2_to_sm_bytes_per_update"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def read_traffic(cfg, kind="pass"):
     path = os.path.join(ROOT, "profiles", f"{kind}_traffic_cfg{cfg}.json")
     if os.path.exists(path):
@@ -679,7 +689,7 @@ def run_oos(args):
         "roofline": {"bound": "l2", "achieved": round(bytes_per_it / it_s / 1e9, 1),
                      "peak": round(l2.value, 1) if l2_ok else None, "unit": "GB/s",
                      "frac": round(bytes_per_it / it_s / 1e9 / l2.value, 4) if l2_ok else None,
-                     "traffic": None,
+                     "traffic": oos_traffic(),
                      "peak_source": f"measured here: L2-resident reads of a {bytes_per_it / 1e6:.0f} "
                                     f"MB buffer (libjofc_probe.so jofc_probe_l2_read)",
                      "per": "rank 0's GPU (its share of the delta rows)",
