@@ -7,16 +7,30 @@
 //   psi_j = sum_k r_k,   xi_j = sum_k (1 - r_k) X^(j)_k,
 // and oos_stress (proj/src/oos.cpp:50-57) needs sum_k (delta_j(k) - dist)^2
 // from the same distances, so one streaming pass over delta yields both
-// (fused like the in-sample pass).  jofc_oos_update_kernel then applies the
-// closed-form corner update (proj/src/oos.cpp:98-111), the commensurability
-// term and the per-point stop rule (proj/src/oos.cpp:221-226).
+// (fused like the in-sample pass); the closed-form corner update
+// (proj/src/oos.cpp:98-111), the commensurability term and the per-point stop
+// rule (proj/src/oos.cpp:221-226) follow.
 //
-// Pass layout: CTA = 8 warps = 8 points of one modality (blockIdx.y) and one
-// of kOosSplits slices of the in-sample range (blockIdx.z); X^(j) streams
-// through two shared-memory chunk buffers (512 rows each, filled by the TMA
-// bulk engine, double buffered) shared by the 8 warps; lanes stride the n
-// in-sample rows (coalesced delta reads, 4 in flight per lane), warp shuffles
-// finish the sums.
+// Kernels (jofc_capi.cu, oos_run):
+//   jofc_oos_solve_kernel    (default) the whole batch solve in ONE launch:
+//                            CTAs own point ranges for every iteration, a
+//                            producer warp streams delta/X chunks through a
+//                            TMA ring, consumer warps run pass, fold and update
+//                            (bottom of this file);
+//   jofc_oos_step_kernel     one fused launch per update (pass of y_t after
+//                            update step t - 1), replayed from CUDA graphs --
+//                            the fallback when the persistent plan does not
+//                            fit, or JOFC_OOS_KERNEL=3;
+//   jofc_oos_pass_kernel / jofc_oos_pass2_kernel + jofc_oos_update_kernel
+//                            the earlier two-kernel forms (JOFC_OOS_KERNEL=1/2,
+//                            comparisons only).
+//
+// Per-update pass layout (jofc_oos_pass_kernel / jofc_oos_step_kernel): CTA =
+// 8 warps = 8 points of one modality (blockIdx.y) and one of kOosSplits slices
+// of the in-sample range (blockIdx.z); X^(j) streams through two shared-memory
+// chunk buffers (512 rows each, filled by the TMA bulk engine, double
+// buffered) shared by the 8 warps; lanes stride the n in-sample rows
+// (coalesced delta reads, 4 in flight per lane), warp shuffles finish the sums.
 #pragma once
 
 #include "jofc_kernels.cuh"
