@@ -1362,7 +1362,11 @@ int oos_launch_persistent(jofc_ctx* c, const OosParams& op) {
     std::fprintf(stderr, "oosp: k %d m %d n %lld D %d: G %d S %d R %d stages %d ncta %d nch %d smem %zu\n",
                  k, m, op.n, D, G, S, R, stages, pp.ncta, pp.nch, bytes);
   jofc_oos_solve_kernel<D><<<pp.ncta, kOospThreads, bytes, c->stream>>>(pp);
-  JOFC_CUDA(cudaGetLastError());
+  const cudaError_t le = cudaGetLastError();
+  if (le == cudaErrorLaunchOutOfResources || le == cudaErrorInvalidConfiguration) {
+    return 1;  // (e.g. shared memory not available at this size: the per-update kernels)
+  }
+  JOFC_CUDA(le);
   ++c->launches;
   return JOFC_OK;
 }
