@@ -153,6 +153,20 @@ int jofc_profile_read(jofc_ctx* ctx, double* pass_ms, uint64_t* pass_launches);
 #define JOFC_FIDELITY_DIRECT 1
 int jofc_set_fidelity_form(jofc_ctx* ctx, int form);
 
+/* Which kernels run an out-of-sample batch (jofc_oos_batch / _step / _stress;
+ * same results to rounding).  AUTO (default): the whole batch as ONE
+ * persistent launch (each CTA owns whole points for every update) when the
+ * batch fills its point slots -- at least Q points per SM and >= 80% of the
+ * slots used (Q = 4 at d <= 4, 2 at d <= 8, 1 above): C5's 1000 points on 148
+ * SMs; smaller batches (a single point of oos_embed, a few hundred points) use
+ * one fused launch per update, which spreads each point over several CTAs.
+ * PERSISTENT / PER_UPDATE force one route (the persistent one still falls
+ * back when its shared-memory plan does not fit). */
+#define JOFC_OOS_AUTO 0
+#define JOFC_OOS_PERSISTENT 1
+#define JOFC_OOS_PER_UPDATE 2
+int jofc_set_oos_route(jofc_ctx* ctx, int route);
+
 /* Multi-GPU: let the caller own the product/exchange buffer (device memory of
  * this context's GPU, >= m*n_pad*d + 1 doubles with n_pad = 64*ceil(n/64)) so
  * that its collective library can reduce it in place.  NULL reverts. */

@@ -81,6 +81,7 @@ _SIGS = {
     "jofc_stress_evaluations": (C.c_int, [_vp, C.POINTER(C.c_uint64)]),
     "jofc_profile": (C.c_int, [_vp, C.c_int]),
     "jofc_set_fidelity_form": (C.c_int, [_vp, C.c_int]),
+    "jofc_set_oos_route": (C.c_int, [_vp, C.c_int]),
     "jofc_profile_read": (C.c_int, [_vp, _dp, C.POINTER(C.c_uint64)]),
     "jofc_set_exchange_buffer": (C.c_int, [_vp, _vp, _sz]),
     "jofc_exchange_count": (_sz, [_vp, _sz]),

@@ -289,6 +289,11 @@ class Device:
         (include/jofc_gpu.h, jofc_set_fidelity_form); True: always per pair."""
         check(self.lib.jofc_set_fidelity_form(self.h, 1 if direct else 0))
 
+    def set_oos_route(self, route: int):
+        """0 auto (default), 1 the persistent batch solve, 2 one fused launch per
+        update (include/jofc_gpu.h, jofc_set_oos_route)."""
+        check(self.lib.jofc_set_oos_route(self.h, int(route)))
+
     def profile(self, enable: bool):
         """CUDA events around every pass launch (also forces per-iteration
         stream launches: no CUDA graph, no single-launch persistent solve)."""

@@ -209,6 +209,7 @@ struct jofc_ctx {
   DevBuf<double> sumsq, sumsq_part;
   DevBuf<double> rho_part;  // epilogue partials of the identity form
   int fidelity_form = JOFC_FIDELITY_AUTO;
+  int oos_route = JOFC_OOS_AUTO;
   int rho_grid = 0;  // epilogue grid of the identity-form solve (its partial rows)
   // solve state (sized for the current d)
   size_t d = 0;

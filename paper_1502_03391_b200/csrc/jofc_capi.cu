@@ -1078,6 +1078,15 @@ int jofc_fjofc_embed(jofc_ctx* c, const jofc_weights* spec, size_t d, const doub
   return rc;
 }
 
+int jofc_set_oos_route(jofc_ctx* c, int route) {
+  if (!c) return set_error(JOFC_EINVAL, "null context");
+  if (route != JOFC_OOS_AUTO && route != JOFC_OOS_PERSISTENT && route != JOFC_OOS_PER_UPDATE)
+    return set_error(JOFC_EINVAL, "oos route %d unknown (0 auto, 1 persistent, 2 per update)",
+                     route);
+  c->oos_route = route;
+  return JOFC_OK;
+}
+
 int jofc_set_fidelity_form(jofc_ctx* c, int form) {
   if (!c) return set_error(JOFC_EINVAL, "null context");
   if (form != JOFC_FIDELITY_AUTO && form != JOFC_FIDELITY_DIRECT)
@@ -1278,7 +1287,7 @@ constexpr int kSmemOptin = 231424;  // 227 KB per CTA less the 1 KB the driver r
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 template <int D>
-int oos_launch_persistent(jofc_ctx* c, const OosParams& op) {
+int oos_launch_persistent(jofc_ctx* c, const OosParams& op, bool auto_route) {
   constexpr int Q = oosp_q<D>();
   constexpr int V = D + 2;
   const int m = op.m, k = op.k;
@@ -1295,6 +1304,16 @@ int oos_launch_persistent(jofc_ctx* c, const OosParams& op) {
   if (g_env > 0) G = static_cast<int>(std::min<long long>(g_env, kOospConsumers * Q));
   int S = 1;  // slots: the smallest divisor of the consumer warps holding G points
   while (S * Q < G || kOospConsumers % S) ++S;
+  // AUTO: only batches that fill the point slots.  A CTA's time per update
+  // is set by its S slots of Q points, used or not, so a half-empty CTA
+  // loses to the per-update kernels, which spread a point over several CTAs
+  // (device time per 100-update solve, m = 2, n = 5000, d = 3: k = 1 1.46 vs
+  // 0.98 ms, k = 300 1.50 vs 1.40, k = 450 1.54 vs 1.76, k = 600 2.36 vs 2.15,
+  // k = 1000 2.42 vs 2.87, k = 2000 4.52 vs 6.03; k = 1, n = 200000 45 vs 22;
+  // scripts/oos_small_k.py)
+  if (auto_route && g_env <= 0 &&
+      (G < Q || static_cast<double>(G) < 0.8 * static_cast<double>(S * Q)))
+    return 1;
   OospParams pp{};
   // fixed part: part, y, warp sums, previous stresses, sums of X, done flags
   const size_t fixed_bytes = static_cast<size_t>(m) * G * V * 8 + 2ull * G * m * D * 8 +
@@ -1434,18 +1453,19 @@ int oos_run(jofc_ctx* c, size_t k, size_t m, size_t n, size_t d, const double* x
   op.max_it = static_cast<int>(max_it);
   op.fixed = fixed;
   int rc = 1;
-  if (oos_kernel_version() == 4) {
+  if (oos_kernel_version() == 4 && c->oos_route != JOFC_OOS_PER_UPDATE) {
+    const bool auto_route = c->oos_route == JOFC_OOS_AUTO;
     switch (d) {
-      case 1: rc = oos_launch_persistent<1>(c, op); break;
-      case 2: rc = oos_launch_persistent<2>(c, op); break;
-      case 3: rc = oos_launch_persistent<3>(c, op); break;
-      case 4: rc = oos_launch_persistent<4>(c, op); break;
-      case 5: rc = oos_launch_persistent<5>(c, op); break;
-      case 6: rc = oos_launch_persistent<6>(c, op); break;
-      case 7: rc = oos_launch_persistent<7>(c, op); break;
-      case 8: rc = oos_launch_persistent<8>(c, op); break;
-      case 9: rc = oos_launch_persistent<9>(c, op); break;
-      default: rc = oos_launch_persistent<10>(c, op); break;
+      case 1: rc = oos_launch_persistent<1>(c, op, auto_route); break;
+      case 2: rc = oos_launch_persistent<2>(c, op, auto_route); break;
+      case 3: rc = oos_launch_persistent<3>(c, op, auto_route); break;
+      case 4: rc = oos_launch_persistent<4>(c, op, auto_route); break;
+      case 5: rc = oos_launch_persistent<5>(c, op, auto_route); break;
+      case 6: rc = oos_launch_persistent<6>(c, op, auto_route); break;
+      case 7: rc = oos_launch_persistent<7>(c, op, auto_route); break;
+      case 8: rc = oos_launch_persistent<8>(c, op, auto_route); break;
+      case 9: rc = oos_launch_persistent<9>(c, op, auto_route); break;
+      default: rc = oos_launch_persistent<10>(c, op, auto_route); break;
     }
     if (rc != JOFC_OK && rc != 1) return rc;
   }

@@ -3,10 +3,6 @@ batch shapes its layout plan branches on, against the oracle's oos loop
 (proj/src/oos.cpp:180-229 per point): one point per CTA, several point slots per
 CTA, more CTAs than SMs (several waves), every d, odd n, zero-distance rows, the
 stop rule, and the fallback to the per-update kernels when the plan does not fit."""
-import os
-import subprocess
-import sys
-
 import numpy as np
 import pytest
 
@@ -22,6 +18,7 @@ X_TOL, S_TOL = 1e-8, 1e-10
 @pytest.fixture(scope="module")
 def dev():
     d = jg.Device(0)
+    d.set_oos_route(1)  # the persistent solve for every shape (AUTO takes it only for full batches)
     yield d
     d.close()
 
@@ -76,25 +73,42 @@ def test_persistent_zero_distance_rows(dev):
 
 
 def test_persistent_matches_per_update_kernels(dev):
-    # the same batch through the per-update fused step kernel (JOFC_OOS_KERNEL=3,
-    # a fresh process: the library reads the switch once)
+    # the same batch through the per-update fused step kernel
     x, od, y0 = batch(11, 400, 2, 600, 3)
     y, tr, it = jg.oos_embed_batch(x, od, 0.5, y0, jg.OosOptions(1e-300, 30), fixed_iterations=True,
                                    device=dev)
-    here = os.path.dirname(os.path.abspath(__file__))
-    np.savez(os.path.join(os.environ.get("TMPDIR", "/tmp"), "oosp_ab.npz"), x=x, od=od, y0=y0)
-    code = (
-        "import numpy as np, os, sys; sys.path.insert(0, %r); import paper_1502_03391_b200 as jg; "
-        "z = np.load(os.path.join(os.environ.get('TMPDIR', '/tmp'), 'oosp_ab.npz')); "
-        "y, tr, it = jg.oos_embed_batch(z['x'], z['od'], 0.5, z['y0'], jg.OosOptions(1e-300, 30), "
-        "fixed_iterations=True, device=jg.Device(0)); "
-        "np.savez(os.path.join(os.environ.get('TMPDIR', '/tmp'), 'oosp_ab_out.npz'), y=y, tr=tr)"
-        % os.path.dirname(here))
-    subprocess.run([sys.executable, "-c", code], check=True,
-                   env=dict(os.environ, JOFC_OOS_KERNEL="3"))
-    z = np.load(os.path.join(os.environ.get("TMPDIR", "/tmp"), "oosp_ab_out.npz"))
-    assert rel_fro(y, z["y"]) < 1e-12
-    assert np.max(np.abs(tr - z["tr"]) / np.abs(z["tr"])) < 1e-12
+    other = jg.Device(0)
+    try:
+        other.set_oos_route(2)
+        y2, tr2, it2 = jg.oos_embed_batch(x, od, 0.5, y0, jg.OosOptions(1e-300, 30),
+                                          fixed_iterations=True, device=other)
+    finally:
+        other.close()
+    assert np.all(it == it2)
+    assert rel_fro(y, y2) < 1e-12
+    assert np.max(np.abs(tr - tr2) / np.abs(tr2)) < 1e-12
+
+
+def test_auto_route_matches(dev):
+    # AUTO picks the persistent solve for a full batch and the per-update
+    # kernels for a small one; both agree with the forced route
+    for k in (2000, 40):
+        x, od, y0 = batch(13 + k, k, 2, 300, 3)
+        y, tr, _ = jg.oos_embed_batch(x, od, 0.5, y0, jg.OosOptions(1e-300, 15),
+                                      fixed_iterations=True, device=dev)
+        other = jg.Device(0)
+        try:
+            ya, tra, _ = jg.oos_embed_batch(x, od, 0.5, y0, jg.OosOptions(1e-300, 15),
+                                            fixed_iterations=True, device=other)
+        finally:
+            other.close()
+        assert rel_fro(y, ya) < 1e-12
+        assert np.max(np.abs(tr - tra) / np.abs(tra)) < 1e-12
+
+
+def test_route_argument_checked(dev):
+    with pytest.raises(ValueError):
+        dev.set_oos_route(7)
 
 
 def test_persistent_falls_back_when_x_chunks_do_not_fit(dev):
