@@ -1282,7 +1282,22 @@ int oos_launch(jofc_ctx* c, const OosParams& op, int steps) {
 // contiguous range of <= G points for the whole solve.  Returns 1 (nothing
 // launched) when the batch does not fit the kernel's shared-memory plan: the
 // caller falls back to the per-update kernels.
-constexpr int kSmemOptin = 231424;  // 227 KB per CTA less the 1 KB the driver reserves
+// Dynamic shared memory a CTA may opt into on this device, less the block
+// the driver reserves per CTA (B200: 232448 - 1024 bytes).
+int smem_optin(int device) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(device);
+  if (it != cache.end()) return it->second;
+  int optin = 0, reserved = 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess)
+    optin = 232448;
+  if (cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device) !=
+      cudaSuccess)
+    reserved = 1024;
+  return cache[device] = optin - reserved;
+}
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -1299,6 +1314,7 @@ int oos_launch_persistent(jofc_ctx* c, const OosParams& op, bool auto_route) {
     const char* e = std::getenv("JOFC_OOSP_G");
     return e ? std::atoll(e) : 0LL;
   }();
+  const int kSmemOptin = smem_optin(c->device);
   JOFC_CUDA(ensure_smem_attr(jofc_oos_solve_kernel<D>, kSmemOptin, c->device));
   int G = static_cast<int>(std::min<long long>((k + c->num_sms - 1) / c->num_sms, kOospConsumers * Q));
   if (g_env > 0) G = static_cast<int>(std::min<long long>(g_env, kOospConsumers * Q));
