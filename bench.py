@@ -219,9 +219,26 @@ def run_ours(args):
     elif world > 1 or (backend and os.environ.get("JOFC_BENCH_NCCL_ONE_RANK") == "1"):
         # the C ABI's own NCCL reduce-scatter + all-gather, in the CUDA graph
         # (JOFC_BENCH_NCCL_ONE_RANK: a one-rank group under torchrun, the test
-        # hook a one-GPU box can run)
-        from paper_1502_03391_b200.dist import attach_nccl_native
-        attach_nccl_native(dev)
+        # hook a one-GPU box can run).  If the C ABI cannot bring NCCL up on
+        # every rank (e.g. no loadable libnccl), all ranks take the Python hook
+        # (torch's NCCL all-reduce) instead, and the line says so.
+        from paper_1502_03391_b200.dist import attach_nccl, attach_nccl_native
+        ok = 1
+        try:
+            attach_nccl_native(dev)
+        except Exception as e:  # noqa: BLE001 (reported, then the fallback)
+            print(f"[bench] C-ABI NCCL exchange unavailable on rank {rank}: {e}; "
+                  f"using the all-reduce hook", file=sys.stderr)
+            ok = 0
+        if world > 1:
+            flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            ok = int(flag.item())
+        if not ok:
+            if world > 1:
+                dev.nccl_release()
+                attach_nccl(dev, wl.d)
+            args.exchange = "hook"
 
     import ctypes as C
     eps, T = 1e-300, wl.iterations
