@@ -254,7 +254,8 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         solve()
-    fetch()
+    if args.warmup > 0:
+        fetch()
 
     def barrier():
         if world > 1:
