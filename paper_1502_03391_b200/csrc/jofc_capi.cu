@@ -1320,36 +1320,44 @@ int oos_launch_persistent(jofc_ctx* c, const OosParams& op, bool auto_route) {
   if (g_env > 0) G = static_cast<int>(std::min<long long>(g_env, kOospConsumers * Q));
   int S = 1;  // slots: the smallest divisor of the consumer warps holding G points
   while (S * Q < G || kOospConsumers % S) ++S;
-  // AUTO: only batches that fill the point slots.  A CTA's time per update
-  // is set by its S slots of Q points, used or not, so a half-empty CTA
-  // loses to the per-update kernels, which spread a point over several CTAs
-  // (device time per 100-update solve, m = 2, n = 5000, d = 3: k = 1 1.46 vs
-  // 0.98 ms, k = 300 1.50 vs 1.40, k = 450 1.54 vs 1.76, k = 600 2.36 vs 2.15,
-  // k = 1000 2.42 vs 2.87, k = 2000 4.52 vs 6.03; k = 1, n = 200000 45 vs 22;
-  // scripts/oos_small_k.py)
-  if (auto_route && g_env <= 0 &&
-      (G < Q || static_cast<double>(G) < 0.8 * static_cast<double>(S * Q)))
-    return 1;
+  const int ncta = (k + G - 1) / G;
+  const int waves = (ncta + c->num_sms - 1) / c->num_sms;
+  // AUTO: only batches that fill the point slots.  A CTA's time per update is
+  // set by its S slots of Q points, used or not, and a second wave of CTAs
+  // doubles it, so the persistent solve pays off only when the batch uses
+  // >= 75% of waves x SMs x S x Q point slots; smaller or ragged batches run
+  // the per-update kernels, which spread a point over several CTAs.  Device
+  // time per 100-update solve, m = 2, n = 5000, d = 3, persistent vs
+  // per-update (scripts/oos_small_k.py): k = 1 1.46 vs 0.98 ms, k = 300 1.50
+  // vs 1.40, k = 450 1.54 vs 1.76, k = 600 2.36 vs 2.15, k = 1000 2.22 vs
+  // 2.87, k = 2000 4.00 vs 6.03, k = 5000 (two waves) 15.1 vs 13.7; k = 1,
+  // n = 200000 45 vs 22.
+  const double used = static_cast<double>(k) /
+                      (static_cast<double>(waves) * c->num_sms * S * Q);
+  if (auto_route && g_env <= 0 && used < 0.75) return 1;
   OospParams pp{};
   // fixed part: part, y, warp sums, previous stresses, sums of X, done flags
   const size_t fixed_bytes = static_cast<size_t>(m) * G * V * 8 + 2ull * G * m * D * 8 +
                              static_cast<size_t>(kOospConsumers) * Q * V * 8 + static_cast<size_t>(G) * 8 +
                              static_cast<size_t>(m) * D * 8 + static_cast<size_t>(G) * 4 + 64;
-  int R = 0, stages = 0;
-  const int lanes_per_slot = 32 * (kOospConsumers / S);  // R a multiple: every lane the same rows
-  for (int r0 : {512, 256, 128, 64}) {
-    if (rows_env && r0 != rows_env) continue;
-    const int r = std::max(lanes_per_slot, r0 / lanes_per_slot * lanes_per_slot);
-    const size_t stage = (static_cast<size_t>(G) * r + static_cast<size_t>(r) * D + 2) * 8;
-    const long long room = static_cast<long long>(kSmemOptin) - 128 - static_cast<long long>(fixed_bytes);
-    const int st = static_cast<int>(std::min<long long>(kOospMaxStages, room / static_cast<long long>(stage)));
-    if (st >= 4 || (st >= 2 && r0 == 64) || (rows_env && st >= 2)) {
-      R = r;
-      stages = st;
-      break;
-    }
-  }
-  if (R == 0) return 1;
+  // Rows per chunk: as large as two ring stages allow, balanced over the
+  // modality pass (the per-chunk cost -- wait, release, refill -- dominates
+  // small chunks: C5 R = 512 x 5 stages 41.1k batch-it/s, 768 x 3 43.3k,
+  // 1024 x 2 44.7k, 1280 x 2 45.4k), a multiple of the lanes of a slot.
+  const int lanes_per_slot = 32 * (kOospConsumers / S);  // every lane the same rows
+  const long long room = static_cast<long long>(kSmemOptin) - 128 - static_cast<long long>(fixed_bytes);
+  const long long row_bytes = (static_cast<long long>(G) + D) * 8;
+  long long r_max = (room / 2 - 16) / row_bytes / lanes_per_slot * lanes_per_slot;
+  if (rows_env > 0) r_max = std::min<long long>(r_max, std::max<long long>(lanes_per_slot, rows_env));
+  if (r_max < lanes_per_slot) return 1;  // (does not fit: the per-update kernels)
+  const long long nch_min = (op.n + r_max - 1) / r_max;
+  const int R = static_cast<int>(std::min<long long>(
+      r_max, ((op.n + nch_min - 1) / nch_min + lanes_per_slot - 1) / lanes_per_slot * lanes_per_slot));
+  const size_t stage_bytes = (static_cast<size_t>(G) * R + static_cast<size_t>(R) * D + 2) * 8;
+  const int stages = static_cast<int>(
+      std::min<long long>(kOospMaxStages, room / static_cast<long long>(stage_bytes)));
+  if (stages < 2) return 1;
+
   pp.x = op.x;
   pp.deltas = op.deltas;
   pp.ystart = op.y0;
@@ -1367,7 +1375,7 @@ int oos_launch_persistent(jofc_ctx* c, const OosParams& op, bool auto_route) {
   pp.fixed = op.fixed;
   pp.G = G;
   pp.S = S;
-  pp.ncta = (k + G - 1) / G;
+  pp.ncta = ncta;
   pp.R = R;
   pp.stages = stages;
   pp.nch = static_cast<int>((op.n + R - 1) / R);
