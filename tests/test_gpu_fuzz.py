@@ -1,0 +1,108 @@
+"""Randomised shapes through every solve route against the oracle (a stand-in for
+the race / bounds checking compute-sanitizer would give: compute-sanitizer is
+closed on this GPU pool).  A ring-phase, barrier or masking slip shows up as a
+mismatch on some shape.  Fixed seed; each case: random m, n, d, weight family
+and start, a short solve through the route the shape takes by default (fused
+epilogue, persistent cooperative launch, per-launch graph with the identity-form
+fidelity) and the out-of-sample batch through both of its routes."""
+import numpy as np
+import pytest
+
+import paper_1502_03391_b200 as jg
+from conftest import rel_fro
+from oracle.oracle import Port, Spec
+
+pytestmark = pytest.mark.gpu
+
+X_TOL, S_TOL = 1e-8, 1e-10
+
+
+@pytest.fixture(scope="module")
+def dev():
+    d = jg.Device(0)
+    yield d
+    d.close()
+
+
+def rand_problem(rng, m, n, p=3):
+    z = rng.normal(size=(n, p))
+    feats = [z + 0.2 * rng.normal(size=(n, p)) for _ in range(m)]
+    delta = np.stack([np.sqrt(((f[:, None, :] - f[None, :, :]) ** 2).sum(-1)) for f in feats])
+    if rng.random() < 0.3:  # a duplicated object: the dist == 0 guard inside a block
+        i, j = rng.integers(0, n, size=2)
+        delta[:, i, :] = delta[:, j, :]
+        delta[:, :, i] = delta[:, :, j]
+        delta[:, i, i] = 0.0
+        delta[:, i, j] = delta[:, j, i] = 0.0
+    return delta
+
+
+def rand_spec(rng, m):
+    kind = rng.integers(0, 3)
+    if kind == 0:
+        w = float(rng.uniform(0.1, 2.0))
+        return jg.WeightSpec.uniform(w), Spec.uniform(w)
+    if kind == 1:
+        within = rng.uniform(0.5, 2.0, size=m)
+        sc = float(rng.uniform(0.5, 1.5))
+        return jg.WeightSpec.product(within, sc), Spec.product(within, sc)
+    a = rng.uniform(0.2, 1.0, size=(m, m))
+    a = 0.5 * (a + a.T)
+    return jg.WeightSpec.general(a), Spec.general_(a)
+
+
+@pytest.mark.parametrize("case", range(64))
+def test_fuzz_in_sample(dev, case):
+    rng = np.random.default_rng(9000 + case)
+    m = int(rng.integers(1, 5))
+    # mostly small (fused / persistent routes), some past the block threshold
+    n = int(rng.choice([2, 3, 63, 64, 65, 127, 128, 129, 300, 517, 1100, 2300]))
+    d = int(rng.integers(1, 11))
+    delta = rand_problem(rng, m, n)
+    spec, sref = rand_spec(rng, m)
+    x0 = rng.normal(size=(m, n, d))
+    its = int(rng.integers(1, 25))
+    opt = jg.SolveOptions(dim=d, eps=1e-300, max_iterations=its, init=jg.InitKind.provided,
+                          init_config=x0)
+    r = jg.fjofc_embed(jg.OmnibusProblem(list(delta)), spec, opt, device=dev)
+    ref = Port().fjofc_embed(delta, sref, x0, 1e-300, its)
+    assert r.iterations == ref.iterations, (m, n, d, its)
+    assert rel_fro(r.config, ref.x) < X_TOL, (m, n, d, its)
+    floor = 1e-13 * abs(ref.trace[0])
+    for a, b in zip(r.stress_trace, ref.trace):
+        assert abs(a - b) <= max(S_TOL * abs(b), floor), (m, n, d, its)
+
+
+@pytest.mark.parametrize("case", range(24))
+@pytest.mark.parametrize("route", [1, 2])
+def test_fuzz_out_of_sample(dev, case, route):
+    rng = np.random.default_rng(9500 + case)
+    m = int(rng.integers(1, 5))
+    n = int(rng.choice([1, 2, 31, 129, 700, 2049]))
+    d = int(rng.integers(1, 11))
+    k = int(rng.choice([1, 7, 150, 700]))
+    x = rng.normal(size=(m, n, d))
+    yt = rng.normal(size=(k, m, d))
+    od = np.abs(np.stack([[np.sqrt(((x[l] - yt[q, l]) ** 2).sum(1)) + 0.05 * rng.normal(size=n)
+                           for l in range(m)] for q in range(k)]))
+    y0 = rng.normal(size=(k, m, d))
+    if k > 1:
+        y0[0] = x[:, 0, :]  # a start exactly on an in-sample row: dist == 0 there
+    w = float(rng.uniform(0.1, 1.5))
+    its = int(rng.integers(1, 20))
+    dev.set_oos_route(route)
+    try:
+        y, tr, it = jg.oos_embed_batch(x, od, w, y0, jg.OosOptions(1e-300, its),
+                                       fixed_iterations=True, device=dev)
+    finally:
+        dev.set_oos_route(0)
+    sample = np.unique(np.linspace(0, k - 1, min(k, 40)).astype(int))
+    yr, trr, itr = Port().oos_batch(x, od[sample], w, y0[sample], 1e-300, its, fixed=True)
+    for j, q in enumerate(sample):
+        assert it[q] == itr[j]
+        assert rel_fro(y[q], yr[j]) < X_TOL, (m, n, d, k, q)
+        # (absolute floor 1e-13 sigma_0: a point that can fit exactly, e.g. n = 1,
+        # ends at rounding-level stress, 0 on one side and ~1e-31 on the other)
+        floor = 1e-13 * abs(trr[j, 0])
+        assert np.all(np.abs(tr[q] - trr[j]) <= np.maximum(S_TOL * np.abs(trr[j]), floor)), \
+            (m, n, d, k, q)
