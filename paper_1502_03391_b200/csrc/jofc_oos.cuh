@@ -793,9 +793,9 @@ __global__ void __launch_bounds__(kOospThreads, 1) jofc_oos_solve_kernel(const O
 
   if (warp == kOospConsumers) {
     // ---- producer: chunk gc (order: iteration, modality, rows) into stage
-    // gc % kSt once the consumers released its previous use; delta segments
-    // start at their first row rounded down to an even index (16-byte
-    // aligned bulk copies)
+    // gc % kSt once the consumers released its previous use: the CTA's G x R
+    // delta block of the permuted copy, then the X^(l) rows (started at the
+    // even index below them: 16-byte aligned bulk copies)
     if (lane != 0) return;
     long long gc = 0;
     int stg = 0;
