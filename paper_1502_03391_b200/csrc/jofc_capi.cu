@@ -222,9 +222,21 @@ int setup_for(jofc_ctx* c) {
   return setup_pass<D>(c->device);
 }
 
+// 256-thread identity-form epilogue for m <= 8 (JOFC_WIDE_SMALL=0: the
+// 1024-thread form, comparisons)
+bool wide_small_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("JOFC_WIDE_SMALL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int D>
 int launch_epi(jofc_ctx* c, const EpiParams& ep) {
-  if (ep.rho && ep.m <= kWideMaxM)
+  if (ep.rho && ep.m <= kWideSmallMaxM && wide_small_enabled())
+    jofc_epilogue_wide_kernel<D, kWideSmallThreads><<<c->rho_grid, kWideSmallThreads, 0, c->stream>>>(ep);
+  else if (ep.rho && ep.m <= kWideMaxM)
     jofc_epilogue_wide_kernel<D><<<c->rho_grid, kWideThreads, 0, c->stream>>>(ep);
   else
     jofc_epilogue_kernel<D><<<c->epi_grid, kEpiThreads, 0, c->stream>>>(ep);
@@ -493,9 +505,13 @@ int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t 
   if (rho_enabled() && c->fidelity_form == JOFC_FIDELITY_AUTO &&
       (c->world == 1 || c->nccl_comm) && !c->peer.active && !pp.fuse_epilogue && c->sumsq.p) {
     const size_t K = 1 + static_cast<size_t>(L.m) * (d + 3);
-    const long long wide_objs = static_cast<long long>(kWideThreads / 32 / L.m) * 32;
+    const int wthreads = (L.m <= kWideSmallMaxM && wide_small_enabled()) ? kWideSmallThreads
+                                                                          : kWideThreads;
+    const long long wide_objs = static_cast<long long>(wthreads / 32 / L.m) * 32;
+    // (one wave of resident CTAs: 2048 / wthreads per SM)
+    const long long max_ctas = static_cast<long long>(c->num_sms) * (2048 / wthreads);
     c->rho_grid = L.m <= kWideMaxM
-                      ? static_cast<int>(std::min<long long>(c->num_sms,
+                      ? static_cast<int>(std::min<long long>(max_ctas,
                                                              (L.n + wide_objs - 1) / wide_objs))
                       : c->epi_grid;
     JOFC_CUDA(c->rho_part.ensure((static_cast<size_t>(c->rho_grid) + 1) * K));
