@@ -505,8 +505,7 @@ int jofc_gpu::capi::prepare_solve(jofc_ctx* c, const jofc_weights* spec, size_t 
   if (rho_enabled() && c->fidelity_form == JOFC_FIDELITY_AUTO &&
       (c->world == 1 || c->nccl_comm) && !c->peer.active && !pp.fuse_epilogue && c->sumsq.p) {
     const size_t K = 1 + static_cast<size_t>(L.m) * (d + 3);
-    const int wthreads = (L.m <= kWideSmallMaxM && wide_small_enabled()) ? kWideSmallThreads
-                                                                          : kWideThreads;
+    const int wthreads = wide_small_enabled() ? wide_threads(L.m) : kWideThreads;
     const long long wide_objs = static_cast<long long>(wthreads / 32 / L.m) * 32;
     // (one wave of resident CTAs: 2048 / wthreads per SM)
     const long long max_ctas = static_cast<long long>(c->num_sms) * (2048 / wthreads);
