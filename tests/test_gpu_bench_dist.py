@@ -81,3 +81,25 @@ def test_bench_torchrun_native_nccl_one_rank():
     assert "C-ABI NCCL" in out["config"]["collective"]
     assert out["config"]["iterations_per_step"] == 100 and out["value"] > 0
     assert out["e2e"]["x_final_rel_diff_vs_device_run"] < 1e-12
+
+
+def test_bench_torchrun_falls_back_when_native_nccl_refuses():
+    # the default exchange asked of a two-rank group on ONE GPU: NCCL itself
+    # refuses the communicator (two ranks on one device), every rank sees
+    # it, and all of them take the all-reduce hook instead -- the bench line
+    # says which collective ran
+    env = dict(os.environ, JOFC_DIST_BACKEND="gloo", JOFC_BENCH_SHARE_GPU="1")
+    env.pop("JOFC_EXCHANGE", None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "5", "--steps", "2",
+           "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "C-ABI NCCL exchange unavailable" in r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["value"] > 0
+    assert "Python hook" in out["config"]["collective"]
+    assert out["e2e"]["x_final_rel_diff_vs_device_run"] < 1e-12
