@@ -1344,8 +1344,8 @@ int oos_launch_persistent(jofc_ctx* c, const OosParams& op, bool auto_route) {
   // the per-update kernels, which spread a point over several CTAs.  Device
   // time per 100-update solve, m = 2, n = 5000, d = 3, persistent vs
   // per-update (scripts/oos_small_k.py): k = 1 1.46 vs 0.98 ms, k = 300 1.50
-  // vs 1.40, k = 450 1.54 vs 1.76, k = 600 2.36 vs 2.15, k = 1000 2.22 vs
-  // 2.87, k = 2000 4.00 vs 6.03, k = 5000 (two waves) 15.1 vs 13.7; k = 1,
+  // vs 1.40, k = 450 1.28 vs 1.76, k = 600 2.36 vs 2.15, k = 1000 2.20 vs
+  // 2.87, k = 2000 3.99 vs 6.03, k = 5000 (two waves) 15.1 vs 13.7; k = 1,
   // n = 200000 45 vs 22.
   const double used = static_cast<double>(k) /
                       (static_cast<double>(waves) * c->num_sms * S * Q);
@@ -1395,14 +1395,6 @@ int oos_launch_persistent(jofc_ctx* c, const OosParams& op, bool auto_route) {
   pp.stages = stages;
   pp.nch = static_cast<int>((op.n + R - 1) / R);
   pp.stage_doubles = static_cast<unsigned>(static_cast<size_t>(G) * R + static_cast<size_t>(R) * D + 2);
-  // delta in ring order (once per batch)
-  const size_t nperm = static_cast<size_t>(pp.ncta) * m * pp.nch * G * R;
-  JOFC_CUDA(c->oos_delta_p.ensure(nperm));
-  pp.dperm = c->oos_delta_p.p;
-  jofc_oos_permute_kernel<<<static_cast<unsigned>(nperm / R), 256, 0, c->stream>>>(
-      op.deltas, c->oos_delta_p.p, k, m, op.n, pp.ncta, G, R, pp.nch);
-  JOFC_CUDA(cudaGetLastError());
-  ++c->launches;
   size_t o = 128;
   pp.off_ring = static_cast<unsigned>(o);
   o += static_cast<size_t>(stages) * pp.stage_doubles * 8;
@@ -1416,6 +1408,14 @@ int oos_launch_persistent(jofc_ctx* c, const OosParams& op, bool auto_route) {
   o += static_cast<size_t>(G) * 8 + static_cast<size_t>(m) * D * 8 + static_cast<size_t>(G) * 4;
   const size_t bytes = align_up(o, 16);
   if (bytes > static_cast<size_t>(kSmemOptin)) return 1;
+  // delta in ring order (once per batch)
+  const size_t nperm = static_cast<size_t>(pp.ncta) * m * pp.nch * G * R;
+  JOFC_CUDA(c->oos_delta_p.ensure(nperm));
+  pp.dperm = c->oos_delta_p.p;
+  jofc_oos_permute_kernel<<<static_cast<unsigned>(nperm / R), 256, 0, c->stream>>>(
+      op.deltas, c->oos_delta_p.p, k, m, op.n, pp.ncta, G, R, pp.nch);
+  JOFC_CUDA(cudaGetLastError());
+  ++c->launches;
   if (std::getenv("JOFC_OOSP_DEBUG"))
     std::fprintf(stderr, "oosp: k %d m %d n %lld D %d: G %d S %d R %d stages %d ncta %d nch %d smem %zu\n",
                  k, m, op.n, D, G, S, R, stages, pp.ncta, pp.nch, bytes);
