@@ -39,6 +39,13 @@ def metric_name(cfg, m, n, d):
     return f"Guttman iterations/s (fJOFC {CONFIG_NAMES[cfg]}: m={m} n={n} d={d})"
 
 
+def workload_label(cfg, m, n, d, w, general_weights, iterations):
+    """config.workload, the same string on both arms."""
+    spec = (f"general(diag {1.0 - w:g}, off {w:g})" if general_weights else f"uniform(w={w:g})")
+    return (f"{CONFIG_NAMES[cfg]} in-sample fJOFC m={m} n={n} d={d} {spec} "
+            f"{iterations} Guttman iterations/solve")
+
+
 def loaded_product_libraries():
     """Product .so files mapped into this process (the reference arm must map none)."""
     try:
@@ -364,8 +371,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md)",
-            "config": {"workload": f"{CONFIG_NAMES[cfg]} in-sample fJOFC m={wl.m} n={wl.n} "
-                                   f"d={wl.d} {spec.describe()} {T} Guttman iterations/step",
+            "config": {"workload": workload_label(cfg, wl.m, wl.n, wl.d, wl.w, wl.general_weights, T),
                        "iterations_per_step": its, "packed_pairs": pairs,
                        "iterations_timed": int(total_its),
                        "inputs": "packed Delta resident in HBM when the timed region starts "
@@ -629,8 +635,8 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": round(sec / args.steps * 1e3, 2),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md)",
-        "config": {"workload": f"{CONFIG_NAMES[cfg]} in-sample fJOFC m={wl.m} n={wl.n} d={wl.d} "
-                               f"{wl.describe_spec()} {wl.iterations} Guttman iterations/solve",
+        "config": {"workload": workload_label(cfg, wl.m, wl.n, wl.d, wl.w, wl.general_weights,
+                                             wl.iterations),
                    "iterations_per_step": per_step,
                    "inputs": "dense host Delta (reference OmnibusProblem), reference Rng X0"},
         "delta_entries_per_s": value * wl.m * wl.n * (wl.n - 1) / 2,

@@ -17,6 +17,9 @@ KERNELS = {
     "jofc_solve_persistent_kernel<3>": "_ZN8jofc_gpu28jofc_solve_persistent_kernelILi3EEEvNS_10PassParamsE",
     "jofc_solve_persistent_kernel<2>": "_ZN8jofc_gpu28jofc_solve_persistent_kernelILi2EEEvNS_10PassParamsE",
     "jofc_epilogue_kernel<5>": "_ZN8jofc_gpu20jofc_epilogue_kernelILi5EEEvNS_9EpiParamsE",
+    "jofc_epilogue_wide_kernel<5,256>": "_ZN8jofc_gpu25jofc_epilogue_wide_kernelILi5ELi256EEEvNS_9EpiParamsE",
+    "jofc_epilogue_wide_kernel<3,1024>": "_ZN8jofc_gpu25jofc_epilogue_wide_kernelILi3ELi1024EEEvNS_9EpiParamsE",
+    "jofc_oos_solve_kernel<3>": "_ZN8jofc_gpu21jofc_oos_solve_kernelILi3EEEvNS_10OospParamsE",
     "jofc_oos_step_kernel<3>": "_ZN8jofc_gpu20jofc_oos_step_kernelILi3EEEvNS_9OosParamsE",
     "jofc_oos_pass_kernel<3>": "_ZN8jofc_gpu20jofc_oos_pass_kernelILi3EEEvNS_9OosParamsE",
 }

@@ -20,6 +20,7 @@ def test_reference_arm_is_product_free_and_comparable():
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference"
     assert line["metric"] == bench.metric_name(1, 2, 500, 2)
+    assert line["config"]["workload"] == bench.workload_label(1, 2, 500, 2, 0.5, True, 100)
     assert line["product_libraries_loaded"] == []
     assert line["e2e"]["value"] == line["value"] and line["unit"] == "it/s"
     assert line["cpu_baseline"]["kind"] in ("reference", "port")
