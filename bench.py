@@ -104,7 +104,8 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+              "power.limit")
 
     def __init__(self, gpu):
         self.gpu = gpu
@@ -125,7 +126,7 @@ class ClockSampler:
         time.sleep(0.15)
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, watts, limit = [], None, set(), [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
@@ -139,8 +140,14 @@ class ClockSampler:
             for nm, v in zip(names, f[4:8]):
                 if v.lower() == "active":
                     reasons.add(nm)
+            try:  # board power beside the clock: a sw_power_cap run is energy-bound
+                watts.append(float(f[2]))
+                limit = float(f[8]) if len(f) > 8 else limit
+            except ValueError:
+                pass
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": float(np.median(watts)) if watts else None, "power_limit_w": limit}
 
 
 def h2d_bytes_dense_upload(m, n, world, rank):
