@@ -147,7 +147,9 @@ class ClockSampler:
                 pass
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
                 "reasons": sorted(reasons), "samples": len(sm),
-                "power_w": float(np.median(watts)) if watts else None, "power_limit_w": limit}
+                "power_w": float(np.median(watts)) if watts else None,
+                "power_w_max": float(np.max(watts)) if watts else None,  # (power.draw lags: ~1 s average)
+                "power_limit_w": limit}
 
 
 def h2d_bytes_dense_upload(m, n, world, rank):
