@@ -33,3 +33,26 @@ def test_default_reference_iterations_at_least_ten():
     import argparse  # noqa: F401
     src = open(os.path.join(ROOT, "bench.py")).read()
     assert '"--ref-iterations", type=int, default=10' in src
+
+
+def test_clock_sampler_parses_clocks_reasons_and_power():
+    """The bench line's `clocks` object from nvidia-smi CSV rows (clocks, power.draw, the
+    four throttle reasons, power.limit)."""
+    class FakeProc:
+        def terminate(self):
+            pass
+
+        def communicate(self, timeout=None):
+            rows = ["1965, 1965, 310.5, 0x0, Not Active, Not Active, Not Active, Not Active, 1000.00",
+                    "1792, 1965, 870.2, 0x4, Not Active, Not Active, Not Active, Active, 1000.00",
+                    "1785, 1965, 990.0, 0x4, Not Active, Not Active, Not Active, Active, 1000.00",
+                    "garbage"]
+            return "\n".join(rows) + "\n", ""
+
+    s = bench.ClockSampler(0)
+    s.proc = FakeProc()
+    out = s.stop()
+    assert out["sm_mhz"] == 1792.0 and out["sm_max_mhz"] == 1965.0 and out["samples"] == 3
+    assert out["reasons"] == ["sw_power_cap"]
+    assert out["power_w"] == 870.2 and out["power_w_max"] == 990.0
+    assert out["power_limit_w"] == 1000.0
