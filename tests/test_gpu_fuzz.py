@@ -15,6 +15,10 @@ from oracle.oracle import Port, Spec
 pytestmark = pytest.mark.gpu
 
 X_TOL, S_TOL = 1e-8, 1e-10
+# JOFC_FUZZ_SEED shifts every case's seed: further sweeps of the same test (the
+# suite itself runs the fixed default)
+import os
+SEED0 = int(os.environ.get("JOFC_FUZZ_SEED", "0"))
 
 
 @pytest.fixture(scope="module")
@@ -53,7 +57,7 @@ def rand_spec(rng, m):
 
 @pytest.mark.parametrize("case", range(64))
 def test_fuzz_in_sample(dev, case):
-    rng = np.random.default_rng(9000 + case)
+    rng = np.random.default_rng(9000 + SEED0 + case)
     m = int(rng.integers(1, 5))
     # mostly small (fused / persistent routes), some past the block threshold
     n = int(rng.choice([2, 3, 63, 64, 65, 127, 128, 129, 300, 517, 1100, 2300]))
@@ -66,9 +70,16 @@ def test_fuzz_in_sample(dev, case):
                           init_config=x0)
     r = jg.fjofc_embed(jg.OmnibusProblem(list(delta)), spec, opt, device=dev)
     ref = Port().fjofc_embed(delta, sref, x0, 1e-300, its)
-    assert r.iterations == ref.iterations, (m, n, d, its)
-    assert rel_fro(r.config, ref.x) < X_TOL, (m, n, d, its)
     floor = 1e-13 * abs(ref.trace[0])
+    if r.iterations != ref.iterations:
+        # Whether the stop rule fires once sigma stagnates at rounding level depends on
+        # the summation order (SURVEY.md 8c rule 5; e.g. n = 2 fits exactly after one
+        # step: 0 -> 0 on one side, 1e-33 -> 0 on the other): the counts may differ only
+        # there, and X and the common prefix of the trace must still agree.
+        t = min(r.iterations, ref.iterations)
+        assert t >= 1 and abs(ref.trace[t] - ref.trace[t - 1]) <= floor, (m, n, d, its)
+        assert abs(r.stress_trace[t] - r.stress_trace[t - 1]) <= floor, (m, n, d, its)
+    assert rel_fro(r.config, ref.x) < X_TOL, (m, n, d, its)
     for a, b in zip(r.stress_trace, ref.trace):
         assert abs(a - b) <= max(S_TOL * abs(b), floor), (m, n, d, its)
 
@@ -76,7 +87,7 @@ def test_fuzz_in_sample(dev, case):
 @pytest.mark.parametrize("case", range(24))
 @pytest.mark.parametrize("route", [1, 2])
 def test_fuzz_out_of_sample(dev, case, route):
-    rng = np.random.default_rng(9500 + case)
+    rng = np.random.default_rng(9500 + SEED0 + case)
     m = int(rng.integers(1, 5))
     n = int(rng.choice([1, 2, 31, 129, 700, 2049]))
     d = int(rng.integers(1, 11))
@@ -86,8 +97,12 @@ def test_fuzz_out_of_sample(dev, case, route):
     od = np.abs(np.stack([[np.sqrt(((x[l] - yt[q, l]) ** 2).sum(1)) + 0.05 * rng.normal(size=n)
                            for l in range(m)] for q in range(k)]))
     y0 = rng.normal(size=(k, m, d))
-    if k > 1:
-        y0[0] = x[:, 0, :]  # a start exactly on an in-sample row: dist == 0 there
+    if k > 1 and n > 1:
+        # a start exactly on an in-sample row: dist == 0 there.  (Not with n = 1: the
+        # update then returns the row itself up to rounding, the next ratio is
+        # delta / 1e-16 and the reference's own iterate is amplified rounding noise --
+        # nothing a different summation order can reproduce.)
+        y0[0] = x[:, 0, :]
     w = float(rng.uniform(0.1, 1.5))
     its = int(rng.integers(1, 20))
     dev.set_oos_route(route)
