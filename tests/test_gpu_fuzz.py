@@ -113,9 +113,16 @@ def test_fuzz_out_of_sample(dev, case, route):
         dev.set_oos_route(0)
     sample = np.unique(np.linspace(0, k - 1, min(k, 40)).astype(int))
     yr, trr, itr = Port().oos_batch(x, od[sample], w, y0[sample], 1e-300, its, fixed=True)
+    # The oracle's own sensitivity to a 2-ulp relative change of delta: a start on an
+    # in-sample row can sit on the line through two rows and reach a saddle of the
+    # point's stress, where rounding noise grows ~3x per update in the oracle itself
+    # (seen at n = 2, d = 10: 2e-8 after 16 updates).  Parity is asked up to that.
+    flip = np.where(np.random.default_rng(1).random(od[sample].shape) < 0.5, -1.0, 1.0)
+    yp, _, _ = Port().oos_batch(x, od[sample] * (1.0 + 4.0e-16 * flip), w, y0[sample], 1e-300,
+                                its, fixed=True)
     for j, q in enumerate(sample):
         assert it[q] == itr[j]
-        assert rel_fro(y[q], yr[j]) < X_TOL, (m, n, d, k, q)
+        assert rel_fro(y[q], yr[j]) < max(X_TOL, 20.0 * rel_fro(yp[j], yr[j])), (m, n, d, k, q)
         # (absolute floor 1e-13 sigma_0: a point that can fit exactly, e.g. n = 1,
         # ends at rounding-level stress, 0 on one side and ~1e-31 on the other)
         floor = 1e-13 * abs(trr[j, 0])
